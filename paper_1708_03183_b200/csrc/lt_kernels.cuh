@@ -1,0 +1,124 @@
+// lt_kernels.cuh — native kernel bodies (the executor's plugin surface).
+//
+// The reference registers Python callables by kernel id (executor.py:46-61;
+// bodies problems.py:49-64).  Here a kernel id names a device function; the
+// executor hands it an access context `C` that resolves each descriptor:
+//   C::rd(d)      const double* of the element's own values      (direct)
+//   C::wr(d)      double*       of the element's own values      (direct W/RW)
+//   C::rdm(d, k)  const double* of the k-th mapped target         (mapped READ)
+//   C::inc(d, k)  double*       contribution slot for target k    (mapped INC / WRITE)
+// Mapped INC/WRITE bodies never touch the target itself: they fill their
+// contribution slot and the executor applies the slots in the reference's
+// sequential order (element ascending, then k) -- no atomics anywhere.
+//
+// Scalar bodies are restated with __dadd_rn/__dmul_rn/__ddiv_rn so no FMA
+// contraction can occur: results are bitwise equal to numpy's.
+#pragma once
+
+#include "lt_internal.cuh"
+
+namespace lt {
+
+enum KernelId : int32_t {
+  K_EDGE_INC = 0,   // problems.py:49-51  verts[k] += x
+  K_CELL_INC,       // problems.py:54-56  v += res for v in verts
+  K_EDGE_READ,      // problems.py:59-60  out = verts[0] + verts[1]
+  K_CELL_READ,      // problems.py:63-64  out = verts[0] + verts[1] + verts[2]
+  K_TOY_K1,         // BASELINE config 1, L1: v_k += a / 3
+  K_TOY_K2,         // BASELINE config 1, L2: e = 0.5 * (v0 + v1)
+  K_TOY_K3,         // BASELINE config 1, L3: a += (e0 + e1 + e2) / 3
+  K_DG_FIRST,       // elastic-wave DG kernels, see lt_dg.cuh
+};
+
+struct KernelInfo {
+  const char *name;
+  int32_t nargs;
+};
+
+// Per-descriptor binding resolved for the device
+struct DArg {
+  double *data;
+  const int32_t *map;   // global map values (nullptr if direct)
+  const int32_t *lmap;  // local map (tile-list order), tiled executor only
+  double *scr;          // untiled: global contribution scratch of this descriptor
+  int32_t arity;
+  int32_t vpe;
+  int32_t mode;
+  int32_t inc_off;      // tiled: offset (doubles) of this descriptor's slots in smem
+};
+
+struct IncPlan {
+  int32_t desc;
+  int32_t pad;
+  const int32_t *gc_off;  // per global chunk: range of unique targets
+  const int32_t *utgt;    // unique target ids
+  const int32_t *ut_off;  // per unique target: range of contributor slots
+  const int32_t *slots;   // contributor slot = pos_in_chunk*arity + k, ascending
+};
+
+struct DLoop {
+  int32_t kernel;
+  int32_t n_desc;
+  int32_t chunk;            // tiled: elements per chunk (<= LT_BLOCK)
+  int32_t n_inc;
+  int32_t use_local;
+  int32_t exec_size;
+  const double *params;
+  const int32_t *offsets;   // tiled: per-tile list offsets
+  const int32_t *elements;  // tiled: concatenated lists
+  const int32_t *chunk_base;
+  IncPlan inc[LT_MAX_INC];
+  DArg a[LT_MAX_DESC];
+};
+
+// ---- scalar bodies -----------------------------------------------------------
+template <class C>
+__device__ __forceinline__ void body_edge_inc(C &c) {
+  const double *x = c.rd(0);
+  const int vpe = c.vpe(1);
+  for (int k = 0; k < c.arity(1); ++k) {
+    double *o = c.inc(1, k);
+    for (int i = 0; i < vpe; ++i) o[i] = x[i];
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void body_sum_read(C &c) {  // edge_read / cell_read
+  double *out = c.wr(0);
+  const int vpe = c.vpe(0);
+  const int a = c.arity(1);
+  for (int i = 0; i < vpe; ++i) {
+    double s = c.rdm(1, 0)[i];
+    for (int k = 1; k < a; ++k) s = __dadd_rn(s, c.rdm(1, k)[i]);
+    out[i] = s;
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void body_toy_k1(C &c) {
+  const double *a = c.rd(0);
+  const int vpe = c.vpe(1);
+  for (int k = 0; k < c.arity(1); ++k) {
+    double *o = c.inc(1, k);
+    for (int i = 0; i < vpe; ++i) o[i] = __ddiv_rn(a[i], 3.0);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void body_toy_k2(C &c) {
+  double *e = c.wr(0);
+  const int vpe = c.vpe(0);
+  for (int i = 0; i < vpe; ++i) e[i] = __dmul_rn(0.5, __dadd_rn(c.rdm(1, 0)[i], c.rdm(1, 1)[i]));
+}
+
+template <class C>
+__device__ __forceinline__ void body_toy_k3(C &c) {
+  double *a = c.wr(0);
+  const int vpe = c.vpe(0);
+  for (int i = 0; i < vpe; ++i) {
+    double s = __dadd_rn(__dadd_rn(c.rdm(1, 0)[i], c.rdm(1, 1)[i]), c.rdm(1, 2)[i]);
+    a[i] = __dadd_rn(a[i], __ddiv_rn(s, 3.0));
+  }
+}
+
+}  // namespace lt
