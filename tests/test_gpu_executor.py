@@ -131,10 +131,14 @@ def test_gpu_nonexec_tile_never_runs():
           "out": lt.Dataset("out", cells, 1, data["out"])}
     for mode in ("sequential", "shared"):
         s = lt.inspect_chain(chain, 3, MODES[mode])
+        osch = O.inspect(chain, 3, mode)
+        assert s.serialize() == osch.serialize()
         d2 = {n: d.copy() for n, d in ds.items()}
         lt.execute_schedule(s, chain, bind, d2, lt.default_registry())
         ref = {n: v.copy() for n, v in data.items()}
-        O.execute_untiled(chain, bind, ref, vpe)
+        O.execute_tiled(osch, chain, bind, ref, vpe)
         for n in ref:
             np.testing.assert_array_equal(d2[n].numpy(), ref[n], err_msg=(mode, n))
-        assert np.all(d2["out"].numpy()[8:] == -7.0)
+        # elements whose inputs depend on non-exec data fall into T_ne and keep values
+        tne = s.tiles[-1]
+        assert np.all(d2["out"].numpy()[tne.iteration_lists[1]] == -7.0)
