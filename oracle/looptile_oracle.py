@@ -326,13 +326,12 @@ KERNELS = {
 }
 
 
-def kernel_table():
+def kernel_table(dg: tuple[int, float] | None = None):
+    """Scalar bodies, plus the DG bodies of degree p with timestep dt if given."""
     table = dict(KERNELS)
-    try:
-        from . import dg_oracle
-    except ImportError:  # imported as a top-level module
-        import dg_oracle  # type: ignore
-    table.update(dg_oracle.kernel_table())
+    if dg is not None:
+        from oracle import dg_oracle
+        table.update(dg_oracle.bodies(*dg))
     return table
 
 

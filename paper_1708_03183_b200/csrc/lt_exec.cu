@@ -92,7 +92,10 @@ struct FlatCtx {  // untiled: element ids, global scratch
   }
 };
 
-template <class C>
+// FAM selects which DG degree is compiled into an instantiation (0: scalar
+// kernels only, 1..4: scalar + DG P, 5: everything) so a P1 chain does not
+// pay the register footprint of P4 bodies.
+template <int FAM, class C>
 __device__ __forceinline__ void dispatch(int kernel, C &c) {
   switch (kernel) {
     case K_EDGE_INC: body_edge_inc(c); break;
@@ -102,7 +105,9 @@ __device__ __forceinline__ void dispatch(int kernel, C &c) {
     case K_TOY_K1: body_toy_k1(c); break;
     case K_TOY_K2: body_toy_k2(c); break;
     case K_TOY_K3: body_toy_k3(c); break;
-    default: dg_dispatch(kernel - K_DG_FIRST, c); break;
+    default:
+      if (FAM > 0) dg_dispatch<FAM>(kernel - K_DG_FIRST, c);
+      break;
   }
 }
 
@@ -127,6 +132,7 @@ __device__ __forceinline__ void apply_chunk(const DLoop &L, const IncPlan &P, in
   }
 }
 
+template <int FAM>
 __global__ void __launch_bounds__(LT_BLOCK) k_fused_tiles(const DLoop *__restrict__ loops,
                                                           int n_loops,
                                                           const int32_t *__restrict__ tile_ids) {
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(LT_BLOCK) k_fused_tiles(const DLoop *__restric
       if (lp < CH && c0 + lp < n) {
         const int gpos = beg + c0 + lp;
         TileCtx cx{L, L.elements[gpos], gpos, lp, smem};
-        dispatch(L.kernel, cx);
+        dispatch<FAM>(L.kernel, cx);
       }
       if (L.n_inc) {
         __syncthreads();
@@ -157,12 +163,47 @@ __global__ void __launch_bounds__(LT_BLOCK) k_fused_tiles(const DLoop *__restric
 }
 
 // ---- untiled executor --------------------------------------------------------------
-__global__ void k_untiled_body(const DLoop *__restrict__ Lp, int n) {
+template <int FAM>
+__global__ void __launch_bounds__(256) k_untiled_body(const DLoop *__restrict__ Lp, int n) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const DLoop &L = *Lp;
   FlatCtx cx{L, e};
-  dispatch(L.kernel, cx);
+  dispatch<FAM>(L.kernel, cx);
+}
+
+// smallest instantiation covering every kernel of the chain
+static int chain_family(const ChainView &cv) {
+  int fam = 0;
+  for (const LoopDesc &L : cv.loops) {
+    if (L.kernel < K_DG_FIRST) continue;
+    const int p = (L.kernel - K_DG_FIRST) / 5 + 1;
+    fam = (fam == 0 || fam == p) ? p : 5;
+  }
+  return fam;
+}
+
+typedef void (*FusedFn)(const DLoop *, int, const int32_t *);
+typedef void (*UntiledFn)(const DLoop *, int);
+static FusedFn fused_fn(int fam) {
+  switch (fam) {
+    case 0: return k_fused_tiles<0>;
+    case 1: return k_fused_tiles<1>;
+    case 2: return k_fused_tiles<2>;
+    case 3: return k_fused_tiles<3>;
+    case 4: return k_fused_tiles<4>;
+    default: return k_fused_tiles<5>;
+  }
+}
+static UntiledFn untiled_fn(int fam) {
+  switch (fam) {
+    case 0: return k_untiled_body<0>;
+    case 1: return k_untiled_body<1>;
+    case 2: return k_untiled_body<2>;
+    case 3: return k_untiled_body<3>;
+    case 4: return k_untiled_body<4>;
+    default: return k_untiled_body<5>;
+  }
 }
 
 __global__ void k_untiled_apply(const DLoop *__restrict__ Lp, int d, const int32_t *inv_off,
@@ -315,7 +356,7 @@ static void build_inc_plan(Ctx &ctx, const lt_schedule *s, int j, const lt_map &
   LT_CK(cudaStreamSynchronize(ctx.stream));
 }
 
-static void validate_bindings(const ChainView &cv, const lt_arg *args) {
+static void validate_bindings(const Ctx &ctx, const ChainView &cv, const lt_arg *args) {
   int a = 0;
   for (size_t j = 0; j < cv.loops.size(); ++j) {
     const LoopDesc &L = cv.loops[j];
@@ -365,6 +406,12 @@ static void validate_bindings(const ChainView &cv, const lt_arg *args) {
                                  "' needs a map of arity " + (kn == "toy_k2" ? "2" : "3"));
     } else {
       dg_validate(L.kernel - K_DG_FIRST, j, cv, L, args + a);
+      const int64_t np_ = dg_param_count(L.kernel - K_DG_FIRST);
+      auto it = ctx.params.find(L.kernel);
+      if (np_ > 0 && (it == ctx.params.end() || it->second.n < np_))
+        fail(LT_E_EXECUTION, "loop " + std::to_string(j) + ": kernel '" + kn +
+                                 "' needs its parameter block (" + std::to_string(np_) +
+                                 " doubles) set with lt_ctx_set_kernel_params");
     }
     // a loop may not increment the same dataset through two descriptors, nor
     // read through a map what it increments (par_loop semantics)
@@ -510,15 +557,16 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   for (int j = 0; j < s->n_loops; ++j)
     if (s->loop_space[j] != cv.loops[j].space || s->lists[j].n != cv.total(cv.loops[j].space))
       fail(LT_E_STALE_SCHEDULE, "schedule was inspected for a different chain");
-  validate_bindings(cv, args);
+  validate_bindings(ctx, cv, args);
   const std::string key = plan_key(cv, args, use_local);
   if (!s->plan || s->plan->key != key) {
     s->plan = build_plan(ctx, s, cv, args, use_local);
     s->plan->key = key;
   }
   ExecPlan &P = *s->plan;
+  FusedFn fn = fused_fn(chain_family(cv));
   if (P.smem_bytes > 48 * 1024)
-    LT_CK(cudaFuncSetAttribute(k_fused_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LT_CK(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)P.smem_bytes));
   int launches = 0, colors = 0;
   int64_t visits = 0;
@@ -527,7 +575,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     if (!((reg == LT_CORE && (phases & LT_PHASE_CORE)) ||
           (reg == LT_BOUNDARY && (phases & LT_PHASE_BOUNDARY))))
       continue;
-    k_fused_tiles<<<P.phases[ph].first, LT_BLOCK, P.smem_bytes, ctx.stream>>>(
+    fn<<<P.phases[ph].first, LT_BLOCK, P.smem_bytes, ctx.stream>>>(
         P.dloops.get(), s->n_loops, P.phases[ph].second.get());
     LT_CK_LAUNCH();
     ++launches;
@@ -583,7 +631,7 @@ void forget_ctx(Ctx *ctx) {
 
 static void execute_untiled(Ctx &ctx, const ChainView &cv, const lt_arg *args,
                             lt_exec_info *info) {
-  validate_bindings(cv, args);
+  validate_bindings(ctx, cv, args);
   int a = 0, launches = 0;
   int64_t visits = 0;
   std::vector<DevBuf<double>> scratch;
@@ -603,12 +651,13 @@ static void execute_untiled(Ctx &ctx, const ChainView &cv, const lt_arg *args,
   }
   LT_CK(cudaMemcpyAsync(dl.get(), host.data(), sizeof(DLoop) * host.size(),
                         cudaMemcpyHostToDevice, ctx.stream));
+  UntiledFn ufn = untiled_fn(chain_family(cv));
   for (size_t j = 0; j < cv.loops.size(); ++j) {
     const LoopDesc &L = cv.loops[j];
     const int64_t n = cv.exec_size(L.space);
     visits += n;
     if (n == 0) continue;
-    k_untiled_body<<<grid_for(n, 256), 256, 0, ctx.stream>>>(dl.get() + j, (int)n);
+    ufn<<<grid_for(n, 256), 256, 0, ctx.stream>>>(dl.get() + j, (int)n);
     LT_CK_LAUNCH();
     ++launches;
     for (int d = 0; d < (int)L.desc.size(); ++d) {

@@ -1,0 +1,377 @@
+"""2D isotropic elastic-wave DG (velocity-stress) as a loop chain.
+
+The paper's application (Seigen elastic-wave timestep, ``PAPER.md:762``) is not
+in the reference (SPEC.md:14 excludes it), so this is the project's own
+discretisation, declared on the loop-chain API and run by
+the native kernels ``dg_{vol,iflux,eflux,minv,axpy}_p{1..4}``:
+
+    rho dv/dt = div(sigma)
+    dsigma/dt = lambda tr(eps(v)) I + 2 mu eps(v)
+
+* Orthonormal modal basis of degree P on the reference triangle
+  (-1,-1),(1,-1),(-1,1) (Gram-Schmidt of monomials, so M_ref = I and the
+  inverse-mass loop is a per-cell scaling by 1/(rho |J|) resp. 1/|J|).
+* Strong form: volume term |J| (r_x S_r + s_x S_s) Q per field; facet term
+  = lift of the flux correction at P+1 Gauss-Legendre points per facet.
+* Upwind (exact Riemann) flux with P/S impedances of both sides; free
+  surface on exterior facets by a mirror state (traction-free).
+* Forward Euler ("axpy update").
+
+Chain per timestep (5 loops, seed = cells):
+  L0 cells    dg_vol    [cgeo R, mat R, u R, s R, ru W, rs W]
+  L1 ifacets  dg_iflux  [fgeo R, mat R@if2c, u R@if2c, s R@if2c, ru I@if2c, rs I@if2c]
+  L2 efacets  dg_eflux  [fgeo R, mat R@ef2c, u R@ef2c, s R@ef2c, ru I@ef2c, rs I@ef2c]
+  L3 cells    dg_minv   [cgeo R, mat R, ru RW, rs RW]
+  L4 cells    dg_axpy   [u RW, s RW, ru R, rs R]                      (param: dt)
+``c2v`` is declared (unused by the loops) so the seed loop has a tile
+adjacency map (SURVEY section 7 "Seed adjacency for DG").
+
+Data layout (element-major, like the reference Dataset): u = [vx(nd), vy(nd)],
+s = [sxx(nd), syy(nd), sxy(nd)], cgeo = [rx, ry, sx, sy, detJ],
+mat = [rho, lambda, mu], fgeo = [nx, ny, |f|/2, face_a, face_b] (face_b = -1 on
+exterior facets).  The operator tables (``dg_tables``) are generated once in
+float64 and are the same arrays the CUDA kernels and the CPU oracle use.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from functools import lru_cache
+
+import numpy as np
+
+from .chain import AccessMode, Descriptor, IterationSpace, Loop, MeshMap, build_chain
+from .mesh import (CELLS, EFACETS, IFACETS, VERTS, Mesh, cell_edge_map, facet_topology,
+                   generate_rect_mesh, renumber)
+
+R, W, I, RW = AccessMode.READ, AccessMode.WRITE, AccessMode.INC, AccessMode.RW
+REF_VERTS = np.array([[-1.0, -1.0], [1.0, -1.0], [-1.0, 1.0]])
+
+
+def n_dofs(p: int) -> int:
+    return (p + 1) * (p + 2) // 2
+
+
+def _monomial_exponents(p):
+    return [(i, d - i) for d in range(p + 1) for i in range(d, -1, -1)]
+
+
+def _monomials(p, r, s):
+    ex = _monomial_exponents(p)
+    v = np.stack([r ** i * s ** j for i, j in ex], axis=-1)
+    dr = np.stack([i * r ** max(i - 1, 0) * s ** j if i else 0 * r for i, j in ex], axis=-1)
+    ds = np.stack([j * r ** i * s ** max(j - 1, 0) if j else 0 * r for i, j in ex], axis=-1)
+    return v, dr, ds
+
+
+def triangle_quadrature(n: int):
+    """Collapsed Gauss-Legendre rule on the reference triangle (n x n points)."""
+    x, w = np.polynomial.legendre.leggauss(n)
+    a, b = np.meshgrid(x, x, indexing="ij")
+    wa, wb = np.meshgrid(w, w, indexing="ij")
+    r = (1 + a) * (1 - b) / 2 - 1
+    s = b
+    wt = wa * wb * (1 - b) / 2
+    return r.ravel(), s.ravel(), wt.ravel()
+
+
+@dataclass(frozen=True)
+class DGTables:
+    p: int
+    nd: int
+    nq: int
+    coef: np.ndarray      # psi = monomials @ coef  (nd x nd)
+    Sr: np.ndarray        # int psi_i d_r psi_j   (nd x nd)
+    Ss: np.ndarray
+    E: np.ndarray         # face traces  (3, nq, nd)
+    LIFT: np.ndarray      # w_q psi_i(face pt) (3, nd, nq)
+
+    def basis(self, r, s):
+        v, dr, ds = _monomials(self.p, np.asarray(r, float), np.asarray(s, float))
+        return v @ self.coef, dr @ self.coef, ds @ self.coef
+
+    def vol_params(self) -> np.ndarray:
+        return np.concatenate([self.Sr.ravel(), self.Ss.ravel()])
+
+    def flux_params(self) -> np.ndarray:
+        return np.concatenate([self.E.ravel(), self.LIFT.ravel()])
+
+
+@lru_cache(maxsize=None)
+def dg_tables(p: int) -> DGTables:
+    if not 1 <= p <= 4:
+        raise ValueError("DG degree must be 1..4")
+    nd = n_dofs(p)
+    r, s, w = triangle_quadrature(p + 3)
+    V, Vr, Vs = _monomials(p, r, s)
+    coef = np.eye(nd)
+    for _ in range(2):  # Gram-Schmidt by Cholesky, repeated once for full accuracy
+        P = V @ coef
+        G = P.T @ (w[:, None] * P)
+        coef = coef @ np.linalg.inv(np.linalg.cholesky(G)).T  # psi = V @ coef orthonormal
+    P, Pr, Ps = V @ coef, Vr @ coef, Vs @ coef
+    Sr = P.T @ (w[:, None] * Pr)
+    Ss = P.T @ (w[:, None] * Ps)
+    nq = p + 1
+    t, wq = np.polynomial.legendre.leggauss(nq)
+    E = np.empty((3, nq, nd))
+    LIFT = np.empty((3, nd, nq))
+    for f in range(3):
+        a, b = REF_VERTS[f], REF_VERTS[(f + 1) % 3]
+        pts = ((1 - t)[:, None] * a + (1 + t)[:, None] * b) / 2
+        Vf, _, _ = _monomials(p, pts[:, 0], pts[:, 1])
+        E[f] = Vf @ coef
+        LIFT[f] = (E[f] * wq[:, None]).T
+    return DGTables(p, nd, nq, coef, Sr, Ss, E, LIFT)
+
+
+# ---- geometry ------------------------------------------------------------------------
+
+def cell_geometry(mesh: Mesh) -> np.ndarray:
+    """Per-cell [rx, ry, sx, sy, detJ] of the affine map from the reference triangle."""
+    X = mesh.vertex_coords[mesh.cells_to_vertices.reshape(-1, 3)]
+    xr = (X[:, 1] - X[:, 0]) / 2
+    xs = (X[:, 2] - X[:, 0]) / 2
+    det = xr[:, 0] * xs[:, 1] - xs[:, 0] * xr[:, 1]
+    if np.any(det <= 0):
+        raise ValueError("cells must be counter-clockwise")
+    return np.stack([xs[:, 1] / det, -xs[:, 0] / det, -xr[:, 1] / det, xr[:, 0] / det, det],
+                    axis=1)
+
+
+def facet_geometry(mesh: Mesh, cells: np.ndarray, faces: np.ndarray,
+                   faces_b: np.ndarray | None = None) -> np.ndarray:
+    """[nx, ny, |f|/2, face_a, face_b] with n outward from the first flank."""
+    tri = mesh.cells_to_vertices.reshape(-1, 3)
+    P0 = mesh.vertex_coords[tri[cells, faces]]
+    P1 = mesh.vertex_coords[tri[cells, (faces + 1) % 3]]
+    d = P1 - P0
+    length = np.hypot(d[:, 0], d[:, 1])
+    out = np.stack([d[:, 1] / length, -d[:, 0] / length, length / 2, faces.astype(float),
+                    -np.ones(len(cells)) if faces_b is None else faces_b.astype(float)], axis=1)
+    return out
+
+
+# ---- problem ---------------------------------------------------------------------------
+
+@dataclass
+class ElasticSetup:
+    """Host-side description of one elastic DG instance (no device state)."""
+
+    p: int
+    mesh: Mesh
+    steps_per_chain: int
+    dt: float
+    spaces: dict
+    maps: dict
+    loops: list
+    bindings: tuple
+    data: dict          # name -> numpy values
+    vpe: dict           # name -> values per element
+    space_of: dict      # dataset -> space name
+    tables: DGTables
+    chain: object = None
+
+    @property
+    def n_cells(self) -> int:
+        return self.mesh.num_cells
+
+    @property
+    def dofs(self) -> int:
+        return self.n_cells * 5 * n_dofs(self.p)
+
+
+def _gaussian_projection(mesh: Mesh, tab: DGTables, centre, sigma: float) -> np.ndarray:
+    """L2 projection of exp(-|x-c|^2 / (2 sigma^2)) on each cell (modal coefficients)."""
+    r, s, w = triangle_quadrature(tab.p + 3)
+    psi, _, _ = tab.basis(r, s)                           # (nqv, nd)
+    X = mesh.vertex_coords[mesh.cells_to_vertices.reshape(-1, 3)]
+    out = np.empty((mesh.num_cells, tab.nd))
+    chunk = 1 << 20
+    lam0, lam1, lam2 = -(r + s) / 2, (1 + r) / 2, (1 + s) / 2
+    for c0 in range(0, mesh.num_cells, chunk):
+        Xc = X[c0:c0 + chunk]
+        x = lam0 * Xc[:, 0, 0:1] + lam1 * Xc[:, 1, 0:1] + lam2 * Xc[:, 2, 0:1]
+        y = lam0 * Xc[:, 0, 1:2] + lam1 * Xc[:, 1, 1:2] + lam2 * Xc[:, 2, 1:2]
+        g = np.exp(-((x - centre[0]) ** 2 + (y - centre[1]) ** 2) / (2 * sigma ** 2))
+        out[c0:c0 + chunk] = (g * w) @ psi
+    return out
+
+
+def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
+                  material="homogeneous", noise_seed: int | None = 1, sigma: float = 8.0,
+                  dt: float | None = None, renumbering: str | None = None,
+                  mesh: Mesh | None = None) -> ElasticSetup:
+    """Build the BASELINE elastic DG instance on an nx x ny right-diagonal mesh (h = 1).
+
+    ``material``: "homogeneous" (rho=1, lambda=2, mu=1) or ("uniform", seed) for
+    per-cell rho, lambda, mu ~ U[1, 2] drawn as rng.uniform(1, 2, (cells, 3)).
+    """
+    tab = dg_tables(p)
+    nd = tab.nd
+    if mesh is None:
+        mesh = renumber(generate_rect_mesh(nx, ny), renumbering)
+    c2e = cell_edge_map(mesh)
+    ft = facet_topology(mesh, c2e)
+    C, Fi, Fe = mesh.num_cells, ft.n_interior, ft.n_exterior
+    spaces = {CELLS: IterationSpace(CELLS, C), IFACETS: IterationSpace(IFACETS, Fi),
+              EFACETS: IterationSpace(EFACETS, Fe), VERTS: IterationSpace(VERTS, mesh.num_vertices)}
+    maps = {
+        "c2v": MeshMap("c2v", spaces[CELLS], spaces[VERTS], 3, mesh.cells_to_vertices),
+        "if2c": MeshMap("if2c", spaces[IFACETS], spaces[CELLS], 2, ft.if2c),
+        "ef2c": MeshMap("ef2c", spaces[EFACETS], spaces[CELLS], 1, ft.ef2c),
+    }
+    # geometry
+    cgeo = cell_geometry(mesh)
+    rows = ft.if2c.reshape(-1, 2)
+    faces = ft.iface.reshape(-1, 2)
+    fig = facet_geometry(mesh, rows[:, 0], faces[:, 0], faces[:, 1])
+    tri = mesh.cells_to_vertices.reshape(-1, 3)
+    # the second flank must traverse the facet in the opposite direction
+    assert np.array_equal(tri[rows[:, 1], faces[:, 1]], tri[rows[:, 0], (faces[:, 0] + 1) % 3])
+    feg = facet_geometry(mesh, ft.ef2c, ft.eface)
+    # material
+    if material == "homogeneous":
+        mat = np.tile([1.0, 2.0, 1.0], (C, 1))
+    else:
+        kind, seed = material
+        assert kind == "uniform"
+        mat = np.random.default_rng(seed).uniform(1.0, 2.0, size=(C, 3))
+    if dt is None:
+        cp = np.sqrt((mat[:, 1] + 2 * mat[:, 2]) / mat[:, 0]).max()
+        dt = 0.1 * 1.0 / (cp * (2 * p + 1))
+    # initial condition: Gaussian pulse at the domain centre on all components
+    X = mesh.vertex_coords
+    centre = ((X[:, 0].min() + X[:, 0].max()) / 2, (X[:, 1].min() + X[:, 1].max()) / 2)
+    g = _gaussian_projection(mesh, tab, centre, sigma)
+    q = np.repeat(g[:, None, :], 5, axis=1)                # (C, 5, nd)
+    if noise_seed is not None:
+        q = q + np.random.default_rng(noise_seed).uniform(-1e-3, 1e-3, size=q.shape)
+    data = {
+        "cgeo": cgeo.ravel(), "mat": mat.ravel(),
+        "u": q[:, 0:2, :].reshape(-1).copy(), "s": q[:, 2:5, :].reshape(-1).copy(),
+        "ru": np.zeros(C * 2 * nd), "rs": np.zeros(C * 3 * nd),
+        "figeo": fig.ravel(), "fegeo": feg.ravel(),
+    }
+    vpe = {"cgeo": 5, "mat": 3, "u": 2 * nd, "s": 3 * nd, "ru": 2 * nd, "rs": 3 * nd,
+           "figeo": 5, "fegeo": 5}
+    space_of = {"cgeo": CELLS, "mat": CELLS, "u": CELLS, "s": CELLS, "ru": CELLS, "rs": CELLS,
+                "figeo": IFACETS, "fegeo": EFACETS}
+    loops, bindings = chain_loops(p, steps_per_chain, spaces, maps)
+    return ElasticSetup(p, mesh, steps_per_chain, float(dt), spaces, maps, loops, bindings,
+                        data, vpe, space_of, tab)
+
+
+def chain_loops(p, steps, spaces, maps, loop_cls=Loop, desc_cls=Descriptor, binding_cls=None,
+                modes=None):
+    """Loops + bindings of ``steps`` timesteps (5 loops each)."""
+    if binding_cls is None:
+        from .executor import KernelBinding as binding_cls
+    m = modes or {"R": R, "W": W, "I": I, "RW": RW}
+    C, FI, FE = spaces[CELLS], spaces[IFACETS], spaces[EFACETS]
+    if2c, ef2c = maps["if2c"], maps["ef2c"]
+    step = [
+        (C, f"dg_vol_p{p}", [(None, "R", "cgeo"), (None, "R", "mat"), (None, "R", "u"),
+                             (None, "R", "s"), (None, "W", "ru"), (None, "W", "rs")]),
+        (FI, f"dg_iflux_p{p}", [(None, "R", "figeo"), (if2c, "R", "mat"), (if2c, "R", "u"),
+                                (if2c, "R", "s"), (if2c, "I", "ru"), (if2c, "I", "rs")]),
+        (FE, f"dg_eflux_p{p}", [(None, "R", "fegeo"), (ef2c, "R", "mat"), (ef2c, "R", "u"),
+                                (ef2c, "R", "s"), (ef2c, "I", "ru"), (ef2c, "I", "rs")]),
+        (C, f"dg_minv_p{p}", [(None, "R", "cgeo"), (None, "R", "mat"), (None, "RW", "ru"),
+                              (None, "RW", "rs")]),
+        (C, f"dg_axpy_p{p}", [(None, "RW", "u"), (None, "RW", "s"), (None, "R", "ru"),
+                              (None, "R", "rs")]),
+    ]
+    loops, bindings = [], []
+    for _ in range(steps):
+        for space, kern, acc in step:
+            loops.append(loop_cls(len(loops), space,
+                                  tuple(desc_cls(mp, m[md]) for mp, md, _ in acc), kern))
+            bindings.append(binding_cls(kern, tuple(n for _, _, n in acc)))
+    return loops, tuple(bindings)
+
+
+def kernel_params(setup: ElasticSetup) -> dict[str, np.ndarray]:
+    """Per-kernel parameter blocks: operator tables and dt."""
+    p, tab = setup.p, setup.tables
+    return {f"dg_vol_p{p}": tab.vol_params(), f"dg_iflux_p{p}": tab.flux_params(),
+            f"dg_eflux_p{p}": tab.flux_params(), f"dg_minv_p{p}": np.zeros(1),
+            f"dg_axpy_p{p}": np.array([setup.dt])}
+
+
+@dataclass
+class ElasticProblem:
+    """Device instance: chain + HBM datasets + registry with installed parameters."""
+
+    setup: ElasticSetup
+    chain: object
+    datasets: dict
+    bindings: tuple
+    registry: object
+    schedules: dict = field(default_factory=dict)
+
+    def install_params(self):
+        from . import _lib
+        for name, prm in kernel_params(self.setup).items():
+            kid, _ = _lib.kernel_lookup(name)
+            _lib.set_kernel_params(kid, prm)
+
+    def inspect(self, ts: int, mode=None):
+        from .inspector import ExecMode, inspect_chain
+        mode = mode or ExecMode.SHARED
+        key = (ts, mode)
+        if key not in self.schedules:
+            self.schedules[key] = inspect_chain(self.chain, ts, mode)
+        return self.schedules[key]
+
+    def run_tiled(self, schedule, n_chains: int = 1, use_local_maps: bool = True):
+        from .executor import execute_schedule
+        self.install_params()
+        for _ in range(n_chains):
+            execute_schedule(schedule, self.chain, self.bindings, self.datasets, self.registry,
+                             use_local_maps=use_local_maps)
+
+    def run_untiled(self, n_chains: int = 1):
+        from .executor import execute_untiled
+        self.install_params()
+        for _ in range(n_chains):
+            execute_untiled(self.chain, self.bindings, self.datasets, self.registry)
+
+
+def elastic_problem(setup: ElasticSetup, depth: int | None = None) -> ElasticProblem:
+    from .executor import Dataset
+    from .problems import default_registry
+    chain = build_chain(tuple(setup.spaces.values()), tuple(setup.maps.values()),
+                        setup.loops, depth or len(setup.loops))
+    setup.chain = chain
+    ds = {n: Dataset(n, setup.spaces[setup.space_of[n]], setup.vpe[n], v)
+          for n, v in setup.data.items()}
+    return ElasticProblem(setup, chain, ds, setup.bindings, default_registry())
+
+
+def compulsory_bytes(chain, bindings, vpe: dict, space_total: dict) -> int:
+    """Algorithmic HBM bytes of one chain execution.
+
+    Every dataset the chain reads before writing is read once, every dataset
+    it writes is written once (float64), and every map a loop uses is read
+    once (int32).  This is the B_chain of DESIGN.md (section "Roofline").
+    """
+    first = {}
+    written = set()
+    maps = {}
+    for loop, b in zip(chain.loops, bindings):
+        for d, name in zip(loop.descriptors, b.args):
+            if name not in first:
+                first[name] = d.mode
+            if d.mode is not AccessMode.READ:
+                written.add(name)
+            if d.map is not None:
+                maps[d.map.name] = d.map.source.total * d.map.arity * 4
+    total = 0
+    for name, mode in first.items():
+        size = space_total[name] * vpe[name] * 8
+        if mode in (AccessMode.READ, AccessMode.RW, AccessMode.INC):
+            total += size
+        if name in written:
+            total += size
+    return total + sum(maps.values())

@@ -7,6 +7,10 @@ PROBLEM = {"fig2": lt.FIG2, "eight": lt.EIGHT_LOOP, "toy": lt.TOY}
 
 
 def build_case(prob: str, dims, ren: str):
+    if prob.startswith("dg"):
+        st, chain = dg_setup(f"{prob}_{dims[0]}x{dims[1]}_{ren}")
+        return st.mesh, (chain, {n: v.copy() for n, v in st.data.items()}, dict(st.vpe),
+                         st.bindings)
     mesh = lt.generate_rect_mesh(*dims)
     if ren == "rcm":
         mesh = lt.rcm_renumber(mesh)
@@ -40,3 +44,18 @@ def host_instantiate(problem, spaces, maps, gids, depth, totals):
     bindings = tuple(KernelBinding(s.kernel, tuple(a.dataset for a in s.accesses))
                      for s in problem.loops)
     return chain, data, vpe, bindings
+
+
+def dg_setup(tag: str):
+    """'dg2s1_8x6_none' -> host ElasticSetup + chain, identical to make_golden's instance."""
+    from paper_1708_03183_b200.dg import elastic_setup
+    from paper_1708_03183_b200.chain import build_chain
+    head, d, ren = tag.split("_")[:3]
+    p, steps = int(head[2]), int(head[4:])
+    dims = tuple(int(v) for v in d.split("x"))
+    st = elastic_setup(dims[0], dims[1], p, steps, noise_seed=1, sigma=max(dims) / 8.0,
+                       renumbering=None if ren == "none" else ren)
+    chain = build_chain(tuple(st.spaces.values()), tuple(st.maps.values()), st.loops,
+                        len(st.loops))
+    st.chain = chain
+    return st, chain

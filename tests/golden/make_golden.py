@@ -196,6 +196,25 @@ def main():
                     for n, d in run.items():
                         values[f"{sname}/tiled/{n}"] = d.values.copy()
 
+    # DG-shaped elastic-wave chain: the builder's numpy bodies in the reference executor
+    for p in (1, 2, 3):
+        for dims, ts, steps in (((4, 4), 8, 1), ((8, 6), 16, 1), ((6, 6), 12, 2)):
+            if p == 3 and dims != (4, 4):
+                continue
+            prob = dg_oracle.build_problem_reference(L, dims, p, steps=steps, seed=1)
+            tag = f"dg{p}s{steps}_{dims[0]}x{dims[1]}_none"
+            fingerprints[tag] = prob.chain.fingerprint
+            run = {n: d.copy() for n, d in prob.datasets.items()}
+            L.execute_untiled(prob.chain, prob.bindings, run, prob.registry)
+            for n in ("u", "s", "ru", "rs"):
+                values[f"{tag}/untiled/{n}"] = run[n].values.copy()
+            for mode in MODES:
+                s = record(f"{tag}_ts{ts}_{mode}", prob.chain, ts, mode, check=False)
+                run = {n: d.copy() for n, d in prob.datasets.items()}
+                L.execute_schedule(s, prob.chain, prob.bindings, run, prob.registry)
+                for n in ("u", "s", "ru", "rs"):
+                    values[f"{tag}_ts{ts}_{mode}/tiled/{n}"] = run[n].values.copy()
+
     # invert_map round trips (seed 2024, 100 random maps)
     rng = np.random.default_rng(2024)
     inv = {}

@@ -1,0 +1,71 @@
+"""Elastic-wave DG on the B200 vs the reference-executor goldens (float64)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_npz, golden_schedules, parse_case
+from cases import dg_setup
+
+import paper_1708_03183_b200 as lt
+from paper_1708_03183_b200.dg import ElasticProblem, elastic_problem
+
+pytestmark = pytest.mark.gpu
+DG_CASES = sorted(c for c in golden_schedules()["schedules"] if c.startswith("dg"))
+MODES = {"sequential": lt.ExecMode.SEQUENTIAL, "shared": lt.ExecMode.SHARED}
+RTOL = 1e-12  # north_star: float64 fields within 1e-12 relative (normwise per field)
+
+
+def rel_err(got, ref):
+    return np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)
+
+
+def problem(tag) -> ElasticProblem:
+    st, _ = dg_setup(tag)
+    return elastic_problem(st)
+
+
+@pytest.mark.parametrize("tag", sorted({c.rsplit("_", 2)[0] for c in DG_CASES}))
+def test_gpu_dg_untiled_vs_reference(tag):
+    pb = problem(tag)
+    pb.run_untiled()
+    ref = golden_npz("values.npz")
+    for n in ("u", "s", "ru", "rs"):
+        assert rel_err(pb.datasets[n].numpy(), ref[f"{tag}/untiled/{n}"]) <= RTOL, n
+
+
+@pytest.mark.parametrize("case", DG_CASES)
+@pytest.mark.parametrize("use_local", [False, True])
+def test_gpu_dg_tiled_vs_reference(case, use_local):
+    tag = case.rsplit("_", 2)[0]
+    _, _, _, ts, mode = parse_case(case)
+    pb = problem(tag)
+    s = lt.inspect_chain(pb.chain, ts, MODES[mode])
+    pb.run_tiled(s, use_local_maps=use_local)
+    ref = golden_npz("values.npz")
+    for n in ("u", "s", "ru", "rs"):
+        assert rel_err(pb.datasets[n].numpy(), ref[f"{case}/tiled/{n}"]) <= RTOL, n
+
+
+@pytest.mark.parametrize("p,steps", [(1, 1), (2, 2), (3, 1), (4, 1)])
+def test_gpu_dg_tiled_equals_untiled_at_scale(p, steps):
+    from paper_1708_03183_b200.dg import elastic_setup
+    st = elastic_setup(48, 40, p, steps, material=("uniform", 3), sigma=6.0)
+    a = elastic_problem(st)
+    a.run_untiled(n_chains=2)
+    for ts, mode in ((64, lt.ExecMode.SHARED), (256, lt.ExecMode.SHARED)):
+        st2 = elastic_setup(48, 40, p, steps, material=("uniform", 3), sigma=6.0)
+        b = elastic_problem(st2)
+        b.run_tiled(lt.inspect_chain(b.chain, ts, mode), n_chains=2)
+        for n in ("u", "s"):
+            assert rel_err(b.datasets[n].numpy(), a.datasets[n].numpy()) <= RTOL, (ts, n)
+
+
+def test_gpu_dg_p4_matches_oracle():
+    from oracle import looptile_oracle as O
+    st, chain = dg_setup("dg4s1_4x4_none")
+    data = {n: v.copy() for n, v in st.data.items()}
+    O.execute_untiled(chain, st.bindings, data, st.vpe, O.kernel_table(dg=(4, st.dt)))
+    pb = elastic_problem(dg_setup("dg4s1_4x4_none")[0])
+    pb.run_tiled(lt.inspect_chain(pb.chain, 8, lt.ExecMode.SHARED))
+    for n in ("u", "s", "ru", "rs"):
+        assert rel_err(pb.datasets[n].numpy(), data[n]) <= RTOL, n
