@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .chain import AccessMode, LoopChain
+from .chain import LoopChain
 from .errors import ExecutionError, StaleScheduleError
 
 THREADS_ENV = "LOOPTILE_THREADS"
@@ -307,6 +307,62 @@ def execute_schedule(schedule, chain: LoopChain, bindings, datasets: dict,
     for name, a, b in zip(ExecutionReport.PHASES, ev[:-1], ev[1:]):
         report.phase_seconds.add_events(name, a, b)
     return report
+
+
+class TiledRunner:
+    """Pre-bound tiled execution of one (schedule, chain, datasets) triple.
+
+    The steady-state form of :func:`execute_schedule` for time-stepping
+    drivers: validation and plan building happen once; ``__call__`` issues
+    the colour-phase launches of both regions (no halo exchange) with no host
+    synchronisation, so it can be captured into a CUDA graph (``graph``).
+    """
+
+    def __init__(self, schedule, chain: LoopChain, bindings, datasets: dict,
+                 registry: KernelRegistry, use_local_maps: bool = True):
+        from . import _lib
+        if schedule.fingerprint != chain.fingerprint:
+            raise StaleScheduleError("schedule was inspected for a different chain")
+        check_bindings(chain, bindings, datasets)
+        self._lib = _lib
+        self.bound = _bind(chain, bindings, datasets, registry)
+        self.handle = schedule.device_handle(chain)
+        self.use_local_maps = use_local_maps
+        info = self()  # builds the execution plan outside any capture
+        self.launches_per_call = info.launches
+
+    def __call__(self):
+        return self._lib.execute(self.handle, self.bound.desc, self.bound.args,
+                                 self._lib.PHASE_CORE | self._lib.PHASE_BOUNDARY,
+                                 self.use_local_maps)
+
+    def graph(self, repeats: int = 1):
+        """CUDA graph replaying ``repeats`` chain executions back to back."""
+        import torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(repeats):
+                self()
+        return g
+
+
+class UntiledRunner:
+    """Pre-bound :func:`execute_untiled` (the GPU "original version" baseline)."""
+
+    def __init__(self, chain: LoopChain, bindings, datasets: dict, registry: KernelRegistry):
+        from . import _lib
+        check_bindings(chain, bindings, datasets)
+        self._lib = _lib
+        self.bound = _bind(chain, bindings, datasets, registry)
+        self.launches_per_call = self().launches
+
+    def __call__(self):
+        return self._lib.execute_untiled(self.bound.desc, self.bound.args)
 
 
 # -- result comparison (executor.py:250-273) ---------------------------------------------
