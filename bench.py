@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (nx, ny, p, steps_per_chain, chains_per_job, material, ts, renumber)
-    2: dict(nx=256, ny=256, p=1, T=1, chains=10, material="homogeneous", ts=256,
+    2: dict(nx=256, ny=256, p=1, T=1, chains=10, material="homogeneous", ts=32,
             workload="elastic DG P1 256x256 (131072 cells), 1 timestep/chain, 10 timesteps"),
     3: dict(nx=2048, ny=2048, p=2, T=2, chains=1, material=("uniform", 2), ts=4096,
             workload="elastic DG P2 2048x2048 (8.4M cells), 2 timesteps/chain, heterogeneous"),
@@ -225,8 +225,9 @@ def main():
         runner = UntiledRunner(pb.chain, pb.bindings, pb.datasets, pb.registry)
         graph = None
     else:
-        runner = TiledRunner(sched, pb.chain, pb.bindings, pb.datasets, pb.registry)
-        graph = runner.graph(cfg["chains"])
+        runner = TiledRunner(sched, pb.chain, pb.bindings, pb.datasets, pb.registry,
+                             repeats=cfg["chains"])
+        graph = runner.graph(1)
 
     def step():
         if graph is not None:
@@ -267,9 +268,10 @@ def main():
     vpe = dict(st.vpe)
     totals = {n: st.spaces[st.space_of[n]].total for n in vpe}
     b_chain = compulsory_bytes(pb.chain, pb.bindings, vpe, totals)
-    launches_per_step = runner.launches_per_call * cfg["chains"]
+    calls_per_step = 1 if graph is not None else cfg["chains"]
+    launches_per_step = runner.launches_per_call * calls_per_step
     avg_launch_s = dev_s / (args.steps * launches_per_step)
-    bytes_per_launch = b_chain / runner.launches_per_call
+    bytes_per_launch = b_chain * cfg["chains"] / launches_per_step
     achieved = bytes_per_launch / avg_launch_s / 1e9
     peak, peak_kind = measured_peaks()
     traffic = None
@@ -323,14 +325,14 @@ def main():
                        "renumber": args.renumber, "mode": "shared",
                        "colors": len(sched.color_order), "rounds": sched.recolor_rounds,
                        "inspect_s": round(inspect_s, 4),
-                       "executor": "untiled" if args.untiled else "fused-tiled",
+                       "executor": "untiled" if args.untiled else runner.executor,
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_chain": b_chain,
-                         "launches_per_chain": runner.launches_per_call},
+                         "launches_per_step": launches_per_step},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,

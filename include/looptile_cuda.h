@@ -138,6 +138,8 @@ typedef struct {
     int32_t launches;    /* kernel launches issued by this call */
     int32_t n_colors;    /* colour phases executed */
     int64_t elements;    /* element visits (sum over loops) */
+    int32_t staged;      /* 0: global-memory tiles, 1: staged per colour, 2: staged dataflow */
+    int32_t smem_bytes;  /* dynamic shared memory per CTA */
 } lt_exec_info;
 
 /* ---- library / context ---------------------------------------------------- */
@@ -196,6 +198,11 @@ int lt_schedule_destroy(lt_schedule *s);
  * the caller brackets them with its halo exchange begin()/end() */
 int lt_execute(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain, const lt_arg *args,
                int32_t phases, int32_t use_local_maps, lt_exec_info *info);
+/* execute_schedule repeated `repeats` times back to back (a time-stepping loop
+ * over the same chain, no halo exchange in between); the dataflow executor
+ * overlaps consecutive repeats tile by tile */
+int lt_execute_repeat(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain, const lt_arg *args,
+                      int32_t repeats, int32_t use_local_maps, lt_exec_info *info);
 /* execute_untiled: loops in order, elements ascending (executor.py:163-169) */
 int lt_execute_untiled(lt_ctx *ctx, const lt_chain *chain, const lt_arg *args,
                        lt_exec_info *info);

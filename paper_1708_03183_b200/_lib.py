@@ -75,7 +75,8 @@ class LtScheduleInfo(C.Structure):
 
 
 class LtExecInfo(C.Structure):
-    _fields_ = [("launches", C.c_int32), ("n_colors", C.c_int32), ("elements", C.c_int64)]
+    _fields_ = [("launches", C.c_int32), ("n_colors", C.c_int32), ("elements", C.c_int64),
+                ("staged", C.c_int32), ("smem_bytes", C.c_int32)]
 
 
 # every symbol the header declares, with (restype, argtypes)
@@ -107,6 +108,8 @@ SIGNATURES = {
     "lt_schedule_destroy": (C.c_int, [_P]),
     "lt_execute": (C.c_int, [_P, _P, C.POINTER(LtChain), C.POINTER(LtArg), C.c_int32,
                              C.c_int32, C.POINTER(LtExecInfo)]),
+    "lt_execute_repeat": (C.c_int, [_P, _P, C.POINTER(LtChain), C.POINTER(LtArg), C.c_int32,
+                                    C.c_int32, C.POINTER(LtExecInfo)]),
     "lt_execute_untiled": (C.c_int, [_P, C.POINTER(LtChain), C.POINTER(LtArg),
                                      C.POINTER(LtExecInfo)]),
     "lt_halo_pack": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int64, _P]),
@@ -358,6 +361,14 @@ def execute(sched: ScheduleHandle, chain_desc: ChainDesc, args, phases: int,
     info = LtExecInfo()
     check(load().lt_execute(sched.ctx.bind_stream(), sched.handle, chain_desc.ref, args,
                             phases, int(bool(use_local_maps)), C.byref(info)))
+    return info
+
+
+def execute_repeat(sched: ScheduleHandle, chain_desc: ChainDesc, args, repeats: int,
+                   use_local_maps: bool) -> LtExecInfo:
+    info = LtExecInfo()
+    check(load().lt_execute_repeat(sched.ctx.bind_stream(), sched.handle, chain_desc.ref, args,
+                                   int(repeats), int(bool(use_local_maps)), C.byref(info)))
     return info
 
 

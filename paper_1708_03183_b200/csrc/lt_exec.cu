@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <tuple>
 
@@ -92,6 +93,34 @@ struct FlatCtx {  // untiled: element ids, global scratch
   }
 };
 
+// staged: every dataset row the tile touches lives in shared memory; slots are
+// footprint-local row indices produced by the plan
+struct StagedCtx {
+  const DLoop &L;
+  int e, pos, lpos;  // pos: position in the tile's list
+  double *smem;
+  double *scratch;
+  const int *base;   // per staged dataset: first double of its rows in smem
+  const int *B;      // tile program in smem
+  const int *sbase;  // per descriptor: base of its slot map in B
+  __device__ int vpe(int d) const { return L.a[d].vpe; }
+  __device__ int arity(int d) const { return L.a[d].arity; }
+  __device__ const double *params() const { return L.params; }
+  __device__ int elem() const { return e; }
+  __device__ double *row(int d, int slot) const {
+    return smem + base[L.a[d].ds] + slot * L.a[d].vpe;
+  }
+  __device__ const double *rd(int d) const { return row(d, B[sbase[d] + pos]); }
+  __device__ double *wr(int d) const { return row(d, B[sbase[d] + pos]); }
+  __device__ const double *rdm(int d, int k) const {
+    return row(d, B[sbase[d] + pos * L.a[d].arity + k]);
+  }
+  __device__ double *inc(int d, int k) const {
+    const DArg &A = L.a[d];
+    return scratch + A.inc_off + (lpos * A.arity + k) * A.vpe;
+  }
+};
+
 // FAM selects which DG degree is compiled into an instantiation (0: scalar
 // kernels only, 1..4: scalar + DG P, 5: everything) so a P1 chain does not
 // pay the register footprint of P4 bodies.
@@ -159,6 +188,297 @@ __global__ void __launch_bounds__(LT_BLOCK) k_fused_tiles(const DLoop *__restric
       }
     }
     __syncthreads();
+  }
+}
+
+// ---- staged tiled executor ------------------------------------------------------------
+// One CTA per tile: gather the tile footprint of every bound dataset into
+// shared memory (coalesced along the ascending footprint rows), run the whole
+// chain on it, store back the rows the tile wrote.  Global traffic per tile is
+// one read of its footprint and one write of its outputs, independent of the
+// chain length; the loops themselves only see shared-memory latency.
+__device__ __forceinline__ void apply_chunk_staged(const DLoop &L, const IncPlan &P, int gc,
+                                                   const double *scratch, double *smem,
+                                                   const int *base) {
+  const DArg &A = L.a[P.desc];
+  const int vpe = A.vpe;
+  double *rows = smem + base[A.ds];
+  const int u0 = P.gc_off[gc], u1 = P.gc_off[gc + 1];
+  const int work = (u1 - u0) * vpe;
+  for (int w = threadIdx.x; w < work; w += blockDim.x) {
+    const int u = u0 + w / vpe, c = w - (w / vpe) * vpe;
+    double *dst = rows + P.utgt[u] * vpe + c;
+    const int s0 = P.ut_off[u], s1 = P.ut_off[u + 1];
+    if (A.mode == LT_INC) {
+      double v = *dst;
+      for (int s = s0; s < s1; ++s) v = __dadd_rn(v, scratch[A.inc_off + P.slots[s] * vpe + c]);
+      *dst = v;
+    } else {
+      *dst = scratch[A.inc_off + P.slots[s1 - 1] * vpe + c];
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem_dst, const void *gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Kernel parameters of the staged executor: lives in the constant bank, so the
+// per-loop descriptor fields every thread reads are uniform broadcasts.
+//
+// Tile program: every executable tile owns a contiguous, 16-byte aligned int32
+// blob in HBM holding everything the tile needs besides the dataset rows:
+//   header   [per space: fp count, fp base]
+//            [per loop: list length, chunk count, slot base per descriptor,
+//                       (gc, ut, uo, sl) bases per apply plan]
+//            [per staged dataset: written-flag base or -1]
+//   sections footprint element ids per space, slot maps per (loop, descriptor),
+//            ordered-gather plans per (loop, map), written flags per dataset.
+// One cp.async.bulk (TMA 1-D bulk copy) brings the blob into shared memory;
+// after it every index the tile touches is a shared-memory access.
+struct StagedParams {
+  int32_t n_loops, n_ds, n_sp, hs;   // hs: header ints
+  int32_t loop_pos[LT_MAX_SLOOPS];   // header position of each loop's block
+  int32_t ds_pos;                    // header position of the written-flag bases
+  int32_t pad;
+  const int32_t *blob;
+  const int64_t *blob_off;           // per tile: first int of its blob
+  const int32_t *blob_len;           // per tile: ints (multiple of 4)
+  StageDS ds[LT_MAX_STAGED];
+  DLoop loops[LT_MAX_SLOOPS];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes,
+                                          uint64_t *bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void apply_plan(const DLoop &L, const IncPlan &P, const int *gc_off,
+                                           const int *utgt, const int *ut_off, const int *slots,
+                                           int c, const double *scratch, double *smem,
+                                           const int *base) {
+  const DArg &A = L.a[P.desc];
+  const int vpe = A.vpe;
+  double *rows = smem + base[A.ds];
+  const int u1 = gc_off[c + 1];
+  const double *sc = scratch + A.inc_off;
+  for (int u = gc_off[c] + threadIdx.x; u < u1; u += LT_SBLOCK) {
+    double *dst = rows + utgt[u] * vpe;
+    const int s0 = ut_off[u], s1 = ut_off[u + 1];
+    if (A.mode == LT_INC) {
+      for (int cc = 0; cc < vpe; ++cc) {
+        double v = dst[cc];
+        for (int s = s0; s < s1; ++s) v = __dadd_rn(v, sc[slots[s] * vpe + cc]);
+        dst[cc] = v;
+      }
+    } else {
+      const double *src = sc + slots[s1 - 1] * vpe;
+      for (int cc = 0; cc < vpe; ++cc) dst[cc] = src[cc];
+    }
+  }
+}
+
+// Run one tile: blob (TMA) -> footprint gather (cp.async) -> every loop on
+// shared memory -> store back the rows the tile wrote.  `phase` is the parity
+// of the CTA's mbarrier for this tile.
+template <int FAM>
+__device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base,
+                                         uint64_t *bar, unsigned phase) {
+  const int tid = threadIdx.x;
+  int *B = reinterpret_cast<int *>(smem);
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of smem
+    bulk_load(B, P.blob + P.blob_off[t], 4u * (unsigned)P.blob_len[t], bar);
+  }
+  mbar_wait(bar, phase);
+  if (tid == 0) {
+    int acc = P.blob_len[t] / 2;  // doubles after the blob (blob_len is a multiple of 4)
+    for (int d = 0; d < P.n_ds; ++d) {
+      base[d] = acc;
+      acc += (B[2 * P.ds[d].sp] * P.ds[d].vpe + 1) & ~1;  // keep every region 16-byte aligned
+    }
+    base[P.n_ds] = acc;
+  }
+  __syncthreads();
+  // gather the footprint rows of every dataset (asynchronous copies, all in flight)
+  for (int d = 0; d < P.n_ds; ++d) {
+    const StageDS &S = P.ds[d];
+    if (!S.load) continue;
+    const int vpe = S.vpe;
+    const int *idx = B + B[2 * S.sp + 1];
+    const int rows = B[2 * S.sp];
+    const double *src = S.data;
+    double *dst = smem + base[d];
+    if ((vpe & 1) == 0) {  // 16-byte rows: base[] offsets are even
+      for (int i = tid; i < rows; i += LT_SBLOCK) {
+        const double *a = src + (size_t)idx[i] * vpe;
+        double *b = dst + i * vpe;
+        for (int c = 0; c < vpe; c += 2) cp_async16(b + c, a + c);
+      }
+    } else {
+      for (int i = tid; i < rows; i += LT_SBLOCK) {
+        const double *a = src + (size_t)idx[i] * vpe;
+        double *b = dst + i * vpe;
+        for (int c = 0; c < vpe; ++c) cp_async8(b + c, a + c);
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  double *scratch = smem + base[P.n_ds];
+  for (int j = 0; j < P.n_loops; ++j) {
+    const DLoop &L = P.loops[j];
+    const int *LH = B + P.loop_pos[j];
+    const int n = LH[0];
+    if (n == 0) continue;
+    const int CH = L.chunk;
+    for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
+      if (tid < CH && c0 + tid < n) {
+        StagedCtx cx{L, 0, c0 + tid, tid, smem, scratch, base, B, LH + 2};
+        dispatch<FAM>(L.kernel, cx);
+      }
+      if (L.n_inc) {
+        __syncthreads();
+        for (int i = 0; i < L.n_inc; ++i) {
+          const int *pb = LH + 2 + L.n_desc + 4 * L.inc[i].plan;
+          apply_plan(L, L.inc[i], B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem,
+                     base);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int d = 0; d < P.n_ds; ++d) {
+    const StageDS &S = P.ds[d];
+    const int wb = B[P.ds_pos + d];
+    if (wb < 0) continue;
+    const int vpe = S.vpe;
+    const int *idx = B + B[2 * S.sp + 1];
+    const int *flag = B + wb;
+    const int rows = B[2 * S.sp];
+    double *dst = S.data;
+    const double *src = smem + base[d];
+    if ((vpe & 1) == 0) {
+      for (int i = tid; i < rows; i += LT_SBLOCK) {
+        if (!flag[i]) continue;
+        double2 *b = reinterpret_cast<double2 *>(dst + (size_t)idx[i] * vpe);
+        const double2 *a = reinterpret_cast<const double2 *>(src + i * vpe);
+        for (int c = 0; c < vpe / 2; ++c) b[c] = a[c];
+      }
+    } else {
+      for (int i = tid; i < rows; i += LT_SBLOCK) {
+        if (!flag[i]) continue;
+        double *b = dst + (size_t)idx[i] * vpe;
+        const double *a = src + i * vpe;
+        for (int c = 0; c < vpe; ++c) b[c] = a[c];
+      }
+    }
+  }
+}
+
+// one colour phase per launch, one CTA per tile
+template <int FAM>
+__global__ void __launch_bounds__(LT_SBLOCK) k_staged_tiles(const __grid_constant__ StagedParams P,
+                                                            const int32_t *__restrict__ tile_ids) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int base[LT_MAX_STAGED + 1];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base, &bar, 0);
+}
+
+// Persistent dataflow executor: CTAs pop tile instances (repeat k, tile) from a
+// queue ordered by (repeat, region, colour, id) and wait only for the
+// overlapping tiles that precede them: an overlapping tile of lower colour must
+// have finished this repeat, any other overlapping tile (and the tile itself)
+// the previous repeat.  Waits only target earlier queue items, which are held
+// by running CTAs, so the schedule cannot deadlock.  Replaces the grid-wide
+// barrier between colour classes by point-to-point tile dependencies.
+struct DataflowArgs {
+  const int32_t *order;    // executable tiles in queue order
+  const int32_t *nbr_off;  // per tile: range in nbr
+  const int32_t *nbr;      // (tile << 1) | earlier-colour flag; includes the tile itself
+  int32_t *done;           // per tile: completed repeats
+  int32_t *queue;          // next item
+  int32_t n_exec;
+  int32_t n_items;
+};
+
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ StagedParams P,
+                                                        const DataflowArgs D) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int base[LT_MAX_STAGED + 1];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int item;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  unsigned phase = 0;
+  for (;;) {
+    if (threadIdx.x == 0) item = atomicAdd(D.queue, 1);
+    __syncthreads();
+    const int it = item;
+    if (it >= D.n_items) return;
+    const int k = it / D.n_exec;
+    const int t = D.order[it - k * D.n_exec];
+    const int n0 = D.nbr_off[t], n1 = D.nbr_off[t + 1];
+    for (int i = n0 + threadIdx.x; i < n1; i += LT_SBLOCK) {
+      const int e = D.nbr[i];
+      const int need = k + (e & 1);
+      const int32_t *flag = D.done + (e >> 1);
+      while (ld_acquire(flag) < need) __nanosleep(32);
+    }
+    __threadfence();  // gpu-scope fence: drop stale L1 lines before gathering
+    __syncthreads();
+    run_tile<FAM>(P, t, smem, base, &bar, phase);
+    phase ^= 1u;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(D.done + t, 1);
   }
 }
 
@@ -276,16 +596,181 @@ struct IncBuffers {
   DevBuf<int32_t> gc_off, utgt, ut_off, slots;
 };
 
+// ---- tile footprints (staged executor plan) ------------------------------------------
+// FP(t, S): ascending unique elements of space S that tile t touches in any loop,
+// directly or through a map.  The extension of compute_local_maps
+// (inspector.py:397-418) that makes tile-local numbering possible.
+struct Footprint {
+  DevBuf<int32_t> off;   // n_tiles + 1
+  DevBuf<int32_t> elem;  // concatenated, ascending per tile
+  DevBuf<uint32_t> tile; // tile of each entry
+  int64_t n = 0;
+  std::vector<int32_t> off_host;
+};
+
+static constexpr uint64_t kNoKey = ~0ull;
+
+__global__ void k_fp_keys_direct(const int32_t *sigma, int64_t n, const int32_t *region,
+                                 uint64_t *keys) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int t = sigma[e];
+  keys[e] = (region[t] == LT_NONEXEC) ? kNoKey : (((uint64_t)t << 32) | (uint32_t)e);
+}
+
+__global__ void k_fp_keys_mapped(const int32_t *sigma, const int32_t *map, int arity, int64_t n,
+                                 const int32_t *region, uint64_t *keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * arity) return;
+  const int t = sigma[i / arity];
+  keys[i] = (region[t] == LT_NONEXEC) ? kNoKey : (((uint64_t)t << 32) | (uint32_t)map[i]);
+}
+
+__global__ void k_fp_heads(const uint64_t *keys, int64_t n, int32_t *heads) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  heads[i] = (keys[i] != kNoKey && (i == 0 || keys[i] != keys[i - 1])) ? 1 : 0;
+}
+
+__global__ void k_fp_fill(const uint64_t *keys, const int32_t *heads, const int32_t *idx,
+                          int64_t n, int32_t *elem, uint32_t *tile) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !heads[i]) return;
+  elem[idx[i]] = (int32_t)(keys[i] & 0xffffffffu);
+  tile[idx[i]] = (uint32_t)(keys[i] >> 32);
+}
+
+__device__ __forceinline__ int fp_slot(const int32_t *fp_off, const int32_t *fp_elem, int t,
+                                       int e) {
+  int lo = fp_off[t], hi = fp_off[t + 1];
+  const int b = lo;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (fp_elem[mid] < e) lo = mid + 1; else hi = mid;
+  }
+  return lo - b;
+}
+
+// slot of each list position (direct) or each (position, k) (mapped); -1 on T_ne
+__global__ void k_slots(const int32_t *elements, const int32_t *sigma, const int32_t *map,
+                        int arity, int64_t n, const int32_t *region, const int32_t *fp_off,
+                        const int32_t *fp_elem, int32_t *slot) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * arity) return;
+  const int e = elements[i / arity];
+  const int t = sigma[e];
+  if (region[t] == LT_NONEXEC) { slot[i] = -1; return; }
+  const int target = map ? map[(int64_t)e * arity + (i % arity)] : e;
+  slot[i] = fp_slot(fp_off, fp_elem, t, target);
+}
+
+__global__ void k_mark_written(const int32_t *elements, const int32_t *sigma, int arity,
+                               int64_t n, const int32_t *fp_off, const int32_t *slot,
+                               uint8_t *flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * arity) return;
+  const int s = slot[i];
+  if (s < 0) return;
+  flag[fp_off[sigma[elements[i / arity]]] + s] = 1;
+}
+
+// unique INC targets of a chunk -> footprint slots of the chunk's tile
+__global__ void k_utgt_to_slot(int32_t *utgt, const uint32_t *run_gc, int64_t R,
+                               const int32_t *gc_tile, const int32_t *fp_off,
+                               const int32_t *fp_elem) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int t = gc_tile[run_gc[r]];
+  utgt[r] = fp_slot(fp_off, fp_elem, t, utgt[r]);
+}
+
+struct FpSource {
+  int loop;
+  int map;  // -1: direct (the loop's own elements)
+};
+
+static void build_footprint(Ctx &ctx, const lt_schedule *s, const ChainView &cv,
+                            const std::vector<FpSource> &src, const DevBuf<int32_t> &region,
+                            Footprint &fp) {
+  int64_t nkeys = 0;
+  for (const FpSource &f : src)
+    nkeys += s->lists[f.loop].n * (f.map < 0 ? 1 : cv.maps[f.map].arity);
+  DevBuf<uint64_t> keys(std::max<int64_t>(nkeys, 1), ctx.stream),
+      sorted(std::max<int64_t>(nkeys, 1), ctx.stream);
+  int64_t at = 0;
+  for (const FpSource &f : src) {
+    const LoopLists &L = s->lists[f.loop];
+    if (f.map < 0) {
+      if (L.n)
+        k_fp_keys_direct<<<grid_for(L.n, 256), 256, 0, ctx.stream>>>(L.sigma.get(), L.n,
+                                                                     region.get(), keys.get() + at);
+      at += L.n;
+    } else {
+      const lt_map &mp = cv.maps[f.map];
+      if (L.n)
+        k_fp_keys_mapped<<<grid_for(L.n * mp.arity, 256), 256, 0, ctx.stream>>>(
+            L.sigma.get(), mp.values, mp.arity, L.n, region.get(), keys.get() + at);
+      at += L.n * mp.arity;
+    }
+    LT_CK_LAUNCH();
+  }
+  if (nkeys) {
+    size_t tmp = 0;
+    LT_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), sorted.get(), (int)nkeys, 0, 64,
+                                         ctx.stream));
+    DevBuf<char> t((int64_t)tmp, ctx.stream);
+    LT_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), sorted.get(), (int)nkeys, 0, 64,
+                                         ctx.stream));
+  }
+  DevBuf<int32_t> heads(std::max<int64_t>(nkeys, 1), ctx.stream),
+      idx(std::max<int64_t>(nkeys, 1), ctx.stream);
+  int64_t U = 0;
+  if (nkeys) {
+    k_fp_heads<<<grid_for(nkeys, 256), 256, 0, ctx.stream>>>(sorted.get(), nkeys, heads.get());
+    LT_CK_LAUNCH();
+    size_t tmp = 0;
+    LT_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, heads.get(), idx.get(), (int)nkeys,
+                                        ctx.stream));
+    DevBuf<char> t((int64_t)tmp, ctx.stream);
+    LT_CK(cub::DeviceScan::ExclusiveSum(t.get(), tmp, heads.get(), idx.get(), (int)nkeys,
+                                        ctx.stream));
+    int32_t li = 0, lh = 0;
+    LT_CK(cudaMemcpyAsync(&li, idx.get() + nkeys - 1, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    LT_CK(cudaMemcpyAsync(&lh, heads.get() + nkeys - 1, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    LT_CK(cudaStreamSynchronize(ctx.stream));
+    U = (int64_t)li + lh;
+  }
+  fp.elem.alloc(std::max<int64_t>(U, 1), ctx.stream);
+  fp.tile.alloc(std::max<int64_t>(U, 1), ctx.stream);
+  fp.n = U;
+  DevBuf<uint32_t> &tile = fp.tile;
+  if (nkeys) {
+    k_fp_fill<<<grid_for(nkeys, 256), 256, 0, ctx.stream>>>(sorted.get(), heads.get(), idx.get(),
+                                                            nkeys, fp.elem.get(), tile.get());
+    LT_CK_LAUNCH();
+  }
+  fp.off.alloc(s->n_tiles + 1, ctx.stream);
+  lower_bound_u32(ctx, tile.get(), U, s->n_tiles, fp.off.get());
+  fp.off_host.resize(s->n_tiles + 1);
+  LT_CK(cudaMemcpyAsync(fp.off_host.data(), fp.off.get(), sizeof(int32_t) * (s->n_tiles + 1),
+                        cudaMemcpyDeviceToHost, ctx.stream));
+  LT_CK(cudaStreamSynchronize(ctx.stream));
+}
+
 struct LoopPlan {
   int chunk = LT_BLOCK;
   int scratch_per_pos = 0;  // doubles
   DevBuf<int32_t> chunk_base;
-  std::vector<IncBuffers> inc;
+  DevBuf<int32_t> gc_tile;  // staged: tile of each global chunk
+  std::vector<IncBuffers> inc;  // per apply plan
   std::vector<int> inc_desc;
+  std::vector<int> plan_map;    // map of each apply plan
+  std::vector<DevBuf<int32_t>> slots;  // staged: per descriptor footprint slots
 };
 
 struct ExecPlan {
   std::string key;
+  bool staged = false;
   std::vector<LoopPlan> loops;
   std::vector<std::pair<int, DevBuf<int32_t>>> phases;  // (#tiles, tile ids) per colour phase
   std::vector<int> phase_region;
@@ -293,20 +778,36 @@ struct ExecPlan {
   DevBuf<DLoop> dloops;
   std::vector<DLoop> host_loops;
   size_t smem_bytes = 0;
+  // staged
+  std::map<int, Footprint> fp;               // per space
+  std::vector<DevBuf<uint8_t>> wflags;        // per staged dataset
+  StagedParams sp;
+  DevBuf<int32_t> region;
+  DevBuf<int32_t> blob, blob_len;
+  DevBuf<int64_t> blob_off;
+  size_t data_max = 0;  // largest per-tile dataset rows (bytes)
+  // dataflow
+  bool dataflow = false;
+  DevBuf<int32_t> order_all, order_core, order_bnd, nbr_off, nbr, done, queue;
+  int n_all = 0, n_core = 0, n_bnd = 0, grid = 0;
 };
 
-static int choose_chunk(int scratch_per_pos, size_t smem_budget) {
-  if (scratch_per_pos == 0) return LT_BLOCK;
+static int choose_chunk(int scratch_per_pos, size_t smem_budget, int block) {
+  if (scratch_per_pos == 0) return block;
   int ch = (int)(smem_budget / (sizeof(double) * (size_t)scratch_per_pos));
-  ch = std::min(ch, LT_BLOCK);
+  ch = std::min(ch, block);
   if (ch >= 32) ch -= ch % 32;
   if (ch < 1) fail(LT_E_EXECUTION, "loop contributions exceed shared memory");
   return ch;
 }
 
+// Ordered-gather plan of one mapped INC/WRITE descriptor: per global chunk the
+// unique targets and, per target, its contributor slots in (element, k) order.
+// With a footprint, targets are converted to tile-local slots.
 static void build_inc_plan(Ctx &ctx, const lt_schedule *s, int j, const lt_map &mp, int CH,
                            const std::vector<int32_t> &chunk_base_host,
-                           const DevBuf<int32_t> &chunk_base, IncBuffers &out) {
+                           const DevBuf<int32_t> &chunk_base, IncBuffers &out,
+                           const Footprint *fp, const DevBuf<int32_t> *gc_tile) {
   const LoopLists &Lj = s->lists[j];
   const int64_t n = Lj.n, nnz = n * mp.arity;
   const int64_t n_gc = chunk_base_host.back();
@@ -352,6 +853,11 @@ static void build_inc_plan(Ctx &ctx, const lt_schedule *s, int j, const lt_map &
   LT_CK_LAUNCH();
   k_set_int<<<1, 1, 0, ctx.stream>>>(out.ut_off.get() + R, (int32_t)nnz);
   LT_CK_LAUNCH();
+  if (fp) {
+    k_utgt_to_slot<<<grid_for(R, 256), 256, 0, ctx.stream>>>(
+        out.utgt.get(), run_gc.get(), R, gc_tile->get(), fp->off.get(), fp->elem.get());
+    LT_CK_LAUNCH();
+  }
   lower_bound_u32(ctx, run_gc.get(), R, n_gc, out.gc_off.get());
   LT_CK(cudaStreamSynchronize(ctx.stream));
 }
@@ -466,34 +972,495 @@ static std::string plan_key(const ChainView &cv, const lt_arg *args, int use_loc
 }
 
 static const size_t kSmemBudget = 96 * 1024;
+static std::string g_last_fit;
+static const size_t kSmemMax = 227 * 1024;
+
+// ---- tile dependency graph of the dataflow executor ---------------------------------
+// Two tiles depend on each other iff their footprints share an element of some
+// space (every RAW/WAR/WAW hazard between tiles needs a shared element).
+__global__ void k_elem_tile_keys(const int32_t *elem, const uint32_t *tile, int64_t n,
+                                 uint64_t *keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((uint64_t)(uint32_t)elem[i] << 32) | tile[i];
+}
+
+__global__ void k_run_start(const uint64_t *keys, int64_t n, int32_t *r0) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  r0[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? (int32_t)i : 0;
+}
+
+__global__ void k_pair_count(const int32_t *r0, int64_t n, int32_t *cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) cnt[i] = 2 * (int32_t)(i - r0[i]);
+}
+
+__global__ void k_pair_emit(const uint64_t *keys, const int32_t *r0, const int32_t *pos,
+                            int64_t n, uint64_t *pairs) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t ti = (uint32_t)keys[i];
+  int64_t o = pos[i];
+  for (int64_t j = r0[i]; j < i; ++j) {
+    const uint32_t tj = (uint32_t)keys[j];
+    pairs[o++] = ((uint64_t)ti << 32) | tj;
+    pairs[o++] = ((uint64_t)tj << 32) | ti;
+  }
+}
+
+__global__ void k_self_pairs(const int32_t *order, int n, uint64_t *pairs) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) pairs[i] = ((uint64_t)(uint32_t)order[i] << 32) | (uint32_t)order[i];
+}
+
+__global__ void k_nbr_fill(const uint64_t *pairs, const int32_t *heads, const int32_t *idx,
+                           int64_t n, const int32_t *color, int32_t *nbr, uint32_t *owner) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !heads[i]) return;
+  const int a = (int)(pairs[i] >> 32), b = (int)(uint32_t)pairs[i];
+  nbr[idx[i]] = (b << 1) | (color[b] < color[a] ? 1 : 0);
+  owner[idx[i]] = (uint32_t)a;
+}
+
+static void exclusive_sum(Ctx &ctx, const int32_t *in, int32_t *out, int64_t n) {
+  size_t tmp = 0;
+  LT_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, ctx.stream));
+  DevBuf<char> t((int64_t)tmp, ctx.stream);
+  LT_CK(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, (int)n, ctx.stream));
+}
+
+static int64_t last_plus(Ctx &ctx, const int32_t *scan, const int32_t *vals, int64_t n) {
+  int32_t a = 0, b = 0;
+  LT_CK(cudaMemcpyAsync(&a, scan + n - 1, 4, cudaMemcpyDeviceToHost, ctx.stream));
+  LT_CK(cudaMemcpyAsync(&b, vals + n - 1, 4, cudaMemcpyDeviceToHost, ctx.stream));
+  LT_CK(cudaStreamSynchronize(ctx.stream));
+  return (int64_t)a + b;
+}
+
+static void build_dependencies(Ctx &ctx, lt_schedule *s, ExecPlan &P) {
+  // queue orders: (region, colour, id)
+  std::vector<int32_t> all, core, bnd;
+  for (int reg : {LT_CORE, LT_BOUNDARY}) {
+    std::vector<int32_t> v;
+    for (int t = 0; t < s->n_tiles; ++t)
+      if (s->region[t] == reg) v.push_back(t);
+    std::stable_sort(v.begin(), v.end(),
+                     [&](int a, int b) { return s->color[a] < s->color[b]; });
+    (reg == LT_CORE ? core : bnd) = v;
+    all.insert(all.end(), v.begin(), v.end());
+  }
+  P.n_all = (int)all.size();
+  P.n_core = (int)core.size();
+  P.n_bnd = (int)bnd.size();
+  auto upload = [&](DevBuf<int32_t> &d, const std::vector<int32_t> &h) {
+    d.alloc(std::max<int64_t>((int64_t)h.size(), 1), ctx.stream);
+    if (!h.empty())
+      LT_CK(cudaMemcpyAsync(d.get(), h.data(), 4 * h.size(), cudaMemcpyHostToDevice, ctx.stream));
+  };
+  upload(P.order_all, all);
+  upload(P.order_core, core);
+  upload(P.order_bnd, bnd);
+  // overlapping tile pairs over every footprint space, plus (t, t)
+  std::vector<DevBuf<uint64_t>> parts;
+  std::vector<int64_t> sizes;
+  for (auto &kv : P.fp) {
+    Footprint &fp = kv.second;
+    const int64_t n = fp.n;
+    if (n == 0) continue;
+    DevBuf<uint64_t> k(n, ctx.stream), ks(n, ctx.stream);
+    k_elem_tile_keys<<<grid_for(n, 256), 256, 0, ctx.stream>>>(fp.elem.get(), fp.tile.get(), n,
+                                                              k.get());
+    LT_CK_LAUNCH();
+    size_t tmp = 0;
+    LT_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k.get(), ks.get(), (int)n, 0, 64,
+                                         ctx.stream));
+    DevBuf<char> tb((int64_t)tmp, ctx.stream);
+    LT_CK(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k.get(), ks.get(), (int)n, 0, 64,
+                                         ctx.stream));
+    DevBuf<int32_t> r0(n, ctx.stream), r0m(n, ctx.stream), cnt(n, ctx.stream), pos(n, ctx.stream);
+    k_run_start<<<grid_for(n, 256), 256, 0, ctx.stream>>>(ks.get(), n, r0.get());
+    LT_CK_LAUNCH();
+    tmp = 0;
+    LT_CK(cub::DeviceScan::InclusiveScan(nullptr, tmp, r0.get(), r0m.get(), cub::Max(), (int)n,
+                                         ctx.stream));
+    DevBuf<char> tb2((int64_t)tmp, ctx.stream);
+    LT_CK(cub::DeviceScan::InclusiveScan(tb2.get(), tmp, r0.get(), r0m.get(), cub::Max(), (int)n,
+                                         ctx.stream));
+    k_pair_count<<<grid_for(n, 256), 256, 0, ctx.stream>>>(r0m.get(), n, cnt.get());
+    LT_CK_LAUNCH();
+    exclusive_sum(ctx, cnt.get(), pos.get(), n);
+    const int64_t total = last_plus(ctx, pos.get(), cnt.get(), n);
+    DevBuf<uint64_t> pairs(std::max<int64_t>(total, 1), ctx.stream);
+    k_pair_emit<<<grid_for(n, 256), 256, 0, ctx.stream>>>(ks.get(), r0m.get(), pos.get(), n,
+                                                         pairs.get());
+    LT_CK_LAUNCH();
+    parts.push_back(std::move(pairs));
+    sizes.push_back(total);
+  }
+  int64_t total = P.n_all;
+  for (int64_t v : sizes) total += v;
+  DevBuf<uint64_t> cat(std::max<int64_t>(total, 1), ctx.stream), srt(std::max<int64_t>(total, 1), ctx.stream);
+  int64_t at = 0;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    if (sizes[i])
+      LT_CK(cudaMemcpyAsync(cat.get() + at, parts[i].get(), 8 * sizes[i], cudaMemcpyDeviceToDevice,
+                            ctx.stream));
+    at += sizes[i];
+  }
+  if (P.n_all) {
+    k_self_pairs<<<grid_for(P.n_all, 256), 256, 0, ctx.stream>>>(P.order_all.get(), P.n_all,
+                                                               cat.get() + at);
+    LT_CK_LAUNCH();
+  }
+  size_t tmp = 0;
+  if (total) {
+    LT_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, cat.get(), srt.get(), (int)total, 0, 64,
+                                         ctx.stream));
+    DevBuf<char> tb((int64_t)tmp, ctx.stream);
+    LT_CK(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, cat.get(), srt.get(), (int)total, 0, 64,
+                                         ctx.stream));
+  }
+  DevBuf<int32_t> heads(std::max<int64_t>(total, 1), ctx.stream), idx(std::max<int64_t>(total, 1), ctx.stream);
+  int64_t U = 0;
+  if (total) {
+    k_run_heads<<<grid_for(total, 256), 256, 0, ctx.stream>>>(srt.get(), total, heads.get());
+    LT_CK_LAUNCH();
+    exclusive_sum(ctx, heads.get(), idx.get(), total);
+    U = last_plus(ctx, idx.get(), heads.get(), total);
+  }
+  DevBuf<int32_t> color(s->n_tiles, ctx.stream);
+  LT_CK(cudaMemcpyAsync(color.get(), s->color.data(), 4 * s->n_tiles, cudaMemcpyHostToDevice,
+                        ctx.stream));
+  P.nbr.alloc(std::max<int64_t>(U, 1), ctx.stream);
+  DevBuf<uint32_t> owner(std::max<int64_t>(U, 1), ctx.stream);
+  if (total) {
+    k_nbr_fill<<<grid_for(total, 256), 256, 0, ctx.stream>>>(srt.get(), heads.get(), idx.get(),
+                                                            total, color.get(), P.nbr.get(),
+                                                            owner.get());
+    LT_CK_LAUNCH();
+  }
+  P.nbr_off.alloc(s->n_tiles + 1, ctx.stream);
+  lower_bound_u32(ctx, owner.get(), U, s->n_tiles, P.nbr_off.get());
+  P.done.alloc(s->n_tiles, ctx.stream);
+  P.queue.alloc(1, ctx.stream);
+  LT_CK(cudaStreamSynchronize(ctx.stream));
+}
+
+// ---- tile programs ------------------------------------------------------------------
+struct Section {
+  const void *src = nullptr;
+  bool u8 = false;
+  std::vector<int64_t> src_off, dst_off;
+  std::vector<int32_t> len, sub;
+};
+
+__global__ void k_seg_copy(const int32_t *src, const int64_t *src_off, const int32_t *len,
+                           const int32_t *sub, int32_t *dst, const int64_t *dst_off, int n) {
+  for (int s = blockIdx.x; s < n; s += gridDim.x) {
+    const int32_t *a = src + src_off[s];
+    int32_t *b = dst + dst_off[s];
+    const int32_t v = sub[s];
+    for (int i = threadIdx.x; i < len[s]; i += blockDim.x) b[i] = a[i] - v;
+  }
+}
+
+__global__ void k_seg_copy_u8(const uint8_t *src, const int64_t *src_off, const int32_t *len,
+                              int32_t *dst, const int64_t *dst_off, int n) {
+  for (int s = blockIdx.x; s < n; s += gridDim.x) {
+    const uint8_t *a = src + src_off[s];
+    int32_t *b = dst + dst_off[s];
+    for (int i = threadIdx.x; i < len[s]; i += blockDim.x) b[i] = a[i];
+  }
+}
+
+template <class T>
+static void to_host(Ctx &ctx, const DevBuf<T> &d, int64_t n, std::vector<T> &h) {
+  h.resize(n);
+  if (n) LT_CK(cudaMemcpyAsync(h.data(), d.get(), sizeof(T) * n, cudaMemcpyDeviceToHost, ctx.stream));
+}
+
+// Lay out and fill the per-tile programs; returns the largest blob in bytes.
+static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPlan &P,
+                          const std::map<int, int> &sp_index, const std::vector<int> &ds_space) {
+  StagedParams &H = P.sp;
+  const int nl = s->n_loops, nt = s->n_tiles;
+  // header layout
+  int hp = 2 * H.n_sp;
+  for (int j = 0; j < nl; ++j) {
+    H.loop_pos[j] = hp;
+    hp += 2 + (int)cv.loops[j].desc.size() + 4 * (int)P.loops[j].plan_map.size();
+  }
+  H.ds_pos = hp;
+  hp += H.n_ds;
+  H.hs = hp;
+  // host copies of the per-tile ranges
+  std::vector<std::vector<int32_t>> off(nl), cb(nl);
+  std::vector<std::vector<std::vector<int32_t>>> gco(nl), uto(nl);
+  for (int j = 0; j < nl; ++j) {
+    to_host(ctx, s->lists[j].offsets, nt + 1, off[j]);
+    if (P.loops[j].chunk_base.get()) to_host(ctx, P.loops[j].chunk_base, nt + 1, cb[j]);
+    gco[j].resize(P.loops[j].inc.size());
+    uto[j].resize(P.loops[j].inc.size());
+    for (size_t p = 0; p < P.loops[j].inc.size(); ++p) {
+      to_host(ctx, P.loops[j].inc[p].gc_off, P.loops[j].inc[p].gc_off.n, gco[j][p]);
+      to_host(ctx, P.loops[j].inc[p].ut_off, P.loops[j].inc[p].ut_off.n, uto[j][p]);
+    }
+  }
+  LT_CK(cudaStreamSynchronize(ctx.stream));
+  std::vector<const Footprint *> fps(H.n_sp);
+  for (auto &kv : sp_index) fps[kv.second] = &P.fp.at(kv.first);
+  // sections in blob order
+  std::vector<Section> secs;
+  auto sec = [&](const void *src, bool u8) -> Section & {
+    secs.emplace_back();
+    secs.back().src = src;
+    secs.back().u8 = u8;
+    return secs.back();
+  };
+  std::vector<int32_t> hdr_host;
+  std::vector<int32_t> blen(nt, 0);
+  std::vector<int64_t> boff(nt, 0);
+  size_t blob_max = 0;
+  int64_t total = 0;
+  // section indices are fixed per chain; create them once
+  std::vector<int> s_sp(H.n_sp), s_wf(H.n_ds, -1);
+  std::vector<std::vector<int>> s_slot(nl), s_plan(nl);
+  const int s_hdr = (int)secs.size();
+  sec(nullptr, false);
+  for (int k = 0; k < H.n_sp; ++k) s_sp[k] = (int)secs.size(), sec(fps[k]->elem.get(), false);
+  for (int j = 0; j < nl; ++j) {
+    for (size_t d = 0; d < cv.loops[j].desc.size(); ++d)
+      s_slot[j].push_back((int)secs.size()), sec(P.loops[j].slots[d].get(), false);
+    for (size_t p = 0; p < P.loops[j].inc.size(); ++p) {
+      s_plan[j].push_back((int)secs.size());
+      sec(P.loops[j].inc[p].gc_off.get(), false);
+      sec(P.loops[j].inc[p].utgt.get(), false);
+      sec(P.loops[j].inc[p].ut_off.get(), false);
+      sec(P.loops[j].inc[p].slots.get(), false);
+    }
+  }
+  for (int k = 0; k < H.n_ds; ++k)
+    if (P.wflags[k].get()) s_wf[k] = (int)secs.size(), sec(P.wflags[k].get(), true);
+  std::vector<int32_t> hdr(H.hs);
+  int n_exec = 0;
+  for (int t = 0; t < nt; ++t) {
+    if (s->region[t] == LT_NONEXEC) continue;
+    ++n_exec;
+    int64_t cur = H.hs;
+    auto put = [&](int si, int64_t src_off, int32_t len, int32_t sub) -> int32_t {
+      Section &S = secs[si];
+      S.src_off.push_back(src_off);
+      S.dst_off.push_back(total + cur);
+      S.len.push_back(len);
+      S.sub.push_back(sub);
+      const int32_t at = (int32_t)cur;
+      cur += len;
+      return at;
+    };
+    std::fill(hdr.begin(), hdr.end(), -1);
+    for (int k = 0; k < H.n_sp; ++k) {
+      const int32_t o = fps[k]->off_host[t], n = fps[k]->off_host[t + 1] - o;
+      hdr[2 * k] = n;
+      hdr[2 * k + 1] = put(s_sp[k], o, n, 0);
+    }
+    for (int j = 0; j < nl; ++j) {
+      const LoopPlan &LP = P.loops[j];
+      int32_t *h = &hdr[H.loop_pos[j]];
+      const int32_t o = off[j][t], n = off[j][t + 1] - o;
+      h[0] = n;
+      h[1] = cb[j].empty() ? 0 : cb[j][t + 1] - cb[j][t];
+      const int nd = (int)cv.loops[j].desc.size();
+      for (int d = 0; d < nd; ++d) {
+        const int ar = cv.loops[j].desc[d].map < 0 ? 1 : cv.maps[cv.loops[j].desc[d].map].arity;
+        h[2 + d] = put(s_slot[j][d], (int64_t)o * ar, n * ar, 0);
+      }
+      for (size_t p = 0; p < LP.inc.size(); ++p) {
+        const int32_t g0 = cb[j][t], nch = cb[j][t + 1] - g0;
+        const int32_t U0 = gco[j][p][g0], U1 = gco[j][p][g0 + nch];
+        const int32_t S0 = uto[j][p][U0], S1 = uto[j][p][U1];
+        const int si = s_plan[j][p];
+        int32_t *q = &h[2 + nd + 4 * p];
+        q[0] = put(si, g0, nch + 1, U0);
+        q[1] = put(si + 1, U0, U1 - U0, 0);
+        q[2] = put(si + 2, U0, U1 - U0 + 1, S0);
+        q[3] = put(si + 3, S0, S1 - S0, 0);
+      }
+    }
+    for (int k = 0; k < H.n_ds; ++k) {
+      if (s_wf[k] < 0) continue;
+      const int sp = H.ds[k].sp;
+      const int32_t o = fps[sp]->off_host[t], n = fps[sp]->off_host[t + 1] - o;
+      hdr[H.ds_pos + k] = put(s_wf[k], o, n, 0);
+    }
+    {  // header section
+      Section &S = secs[s_hdr];
+      S.src_off.push_back((int64_t)hdr_host.size());
+      S.dst_off.push_back(total);
+      S.len.push_back(H.hs);
+      S.sub.push_back(0);
+      hdr_host.insert(hdr_host.end(), hdr.begin(), hdr.end());
+    }
+    cur = (cur + 3) / 4 * 4;  // 16-byte aligned blobs
+    blen[t] = (int32_t)cur;
+    boff[t] = total;
+    total += cur;
+    blob_max = std::max(blob_max, (size_t)cur * 4);
+  }
+  P.blob.alloc(std::max<int64_t>(total, 4), ctx.stream);
+  P.blob_off.alloc(nt, ctx.stream);
+  P.blob_len.alloc(nt, ctx.stream);
+  LT_CK(cudaMemcpyAsync(P.blob_off.get(), boff.data(), 8 * nt, cudaMemcpyHostToDevice, ctx.stream));
+  LT_CK(cudaMemcpyAsync(P.blob_len.get(), blen.data(), 4 * nt, cudaMemcpyHostToDevice, ctx.stream));
+  DevBuf<int32_t> hdr_dev(std::max<int64_t>((int64_t)hdr_host.size(), 1), ctx.stream);
+  if (!hdr_host.empty())
+    LT_CK(cudaMemcpyAsync(hdr_dev.get(), hdr_host.data(), 4 * hdr_host.size(),
+                          cudaMemcpyHostToDevice, ctx.stream));
+  secs[s_hdr].src = hdr_dev.get();
+  for (Section &S : secs) {
+    const int n = (int)S.len.size();
+    if (n == 0) continue;
+    DevBuf<int64_t> so(n, ctx.stream), dof(n, ctx.stream);
+    DevBuf<int32_t> ln(n, ctx.stream), sb(n, ctx.stream);
+    LT_CK(cudaMemcpyAsync(so.get(), S.src_off.data(), 8 * n, cudaMemcpyHostToDevice, ctx.stream));
+    LT_CK(cudaMemcpyAsync(dof.get(), S.dst_off.data(), 8 * n, cudaMemcpyHostToDevice, ctx.stream));
+    LT_CK(cudaMemcpyAsync(ln.get(), S.len.data(), 4 * n, cudaMemcpyHostToDevice, ctx.stream));
+    LT_CK(cudaMemcpyAsync(sb.get(), S.sub.data(), 4 * n, cudaMemcpyHostToDevice, ctx.stream));
+    const int grid = std::min(n, 65535);
+    if (S.u8)
+      k_seg_copy_u8<<<grid, 128, 0, ctx.stream>>>((const uint8_t *)S.src, so.get(), ln.get(),
+                                                  P.blob.get(), dof.get(), n);
+    else
+      k_seg_copy<<<grid, 128, 0, ctx.stream>>>((const int32_t *)S.src, so.get(), ln.get(), sb.get(),
+                                               P.blob.get(), dof.get(), n);
+    LT_CK_LAUNCH();
+    LT_CK(cudaStreamSynchronize(ctx.stream));
+  }
+  (void)n_exec;
+  (void)ds_space;
+  return blob_max;
+}
+
+// Which executor: LT_EXEC=global (tiles read global memory, one launch per
+// colour), staged (footprints in shared memory, one launch per colour) or
+// dataflow (staged, one persistent launch with tile dependencies).  Default:
+// dataflow when the largest tile footprint fits shared memory, else global.
+static int exec_preference() {
+  const char *e = getenv("LT_EXEC");
+  if (!e) return 0;
+  if (!strcmp(e, "global")) return -1;
+  if (!strcmp(e, "staged")) return 1;
+  if (!strcmp(e, "dataflow")) return 2;
+  return 0;
+}
+
+// Footprints, slot maps and written flags of the staged executor.  Returns
+// false (and leaves the plan untouched) when a footprint exceeds shared memory.
+static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_arg *args,
+                        ExecPlan &P, std::vector<int> &ds_of, std::vector<int> &ds_space,
+                        std::vector<int> &ds_vpe, std::vector<double *> &ds_ptr,
+                        size_t &regions_max) {
+  const int nl = s->n_loops;
+  if (nl > LT_MAX_SLOOPS) return false;
+  // distinct datasets by device pointer
+  int a = 0;
+  for (int j = 0; j < nl; ++j) {
+    for (size_t d = 0; d < cv.loops[j].desc.size(); ++d, ++a) {
+      const lt_desc &D = cv.loops[j].desc[d];
+      const int space = D.map < 0 ? cv.loops[j].space : cv.maps[D.map].target;
+      int found = -1;
+      for (size_t k = 0; k < ds_ptr.size(); ++k)
+        if (ds_ptr[k] == args[a].values) found = (int)k;
+      if (found < 0) {
+        if ((int)ds_ptr.size() >= LT_MAX_STAGED) return false;
+        found = (int)ds_ptr.size();
+        ds_ptr.push_back(args[a].values);
+        ds_space.push_back(space);
+        ds_vpe.push_back(args[a].vpe);
+      }
+      ds_of.push_back(found);
+    }
+  }
+  P.region.alloc(s->n_tiles, ctx.stream);
+  LT_CK(cudaMemcpyAsync(P.region.get(), s->region.data(), sizeof(int32_t) * s->n_tiles,
+                        cudaMemcpyHostToDevice, ctx.stream));
+  // footprints per space touched by a dataset
+  std::map<int, std::vector<FpSource>> sources;
+  for (int j = 0; j < nl; ++j) {
+    std::vector<int> seen;
+    bool direct = false;
+    for (const lt_desc &D : cv.loops[j].desc) {
+      if (D.map < 0) {
+        direct = true;
+      } else if (std::find(seen.begin(), seen.end(), D.map) == seen.end()) {
+        seen.push_back(D.map);
+        sources[cv.maps[D.map].target].push_back({j, D.map});
+      }
+    }
+    if (direct) sources[cv.loops[j].space].push_back({j, -1});
+  }
+  if (sources.size() > LT_MAX_SPACES) return false;
+  for (auto &kv : sources) build_footprint(ctx, s, cv, kv.second, P.region, P.fp[kv.first]);
+  // shared-memory regions of the largest tile: footprint ids + dataset rows
+  regions_max = 0;
+  for (int t = 0; t < s->n_tiles; ++t) {
+    if (s->region[t] == LT_NONEXEC) continue;
+    size_t r = 0;
+    for (size_t k = 0; k < ds_ptr.size(); ++k) {
+      const auto &oh = P.fp[ds_space[k]].off_host;
+      r += (size_t)(oh[t + 1] - oh[t]) * ds_vpe[k];
+    }
+    regions_max = std::max(regions_max, r * sizeof(double));
+  }
+  P.data_max = regions_max + 8 * ds_ptr.size();  // 16-byte alignment padding per region
+  return regions_max + 16 * 1024 <= kSmemMax;
+}
 
 static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const ChainView &cv,
-                                            const lt_arg *args, int use_local) {
+                                            const lt_arg *args, int use_local,
+                                            bool force_global = false) {
   auto plan = std::make_shared<ExecPlan>();
+  ExecPlan &P = *plan;
   const int nl = s->n_loops;
-  plan->loops.resize(nl);
-  plan->host_loops.resize(nl);
+  P.loops.resize(nl);
+  P.host_loops.resize(nl);
+  std::vector<int> ds_of, ds_space, ds_vpe;
+  std::vector<double *> ds_ptr;
+  size_t regions_max = 0;
+  const int pref = force_global ? -1 : exec_preference();
+  if (pref >= 0) {
+    P.staged = build_stage(ctx, s, cv, args, P, ds_of, ds_space, ds_vpe, ds_ptr, regions_max);
+    if (!P.staged && pref > 0)
+      fail(LT_E_EXECUTION, "LT_EXEC=staged/dataflow: tile footprint rows " +
+                               std::to_string(P.data_max) + " B exceed shared memory");
+    if (!P.staged) P.fp.clear();
+    P.dataflow = P.staged && pref != 1;
+  }
+  const int block = P.staged ? LT_SBLOCK : LT_BLOCK;
+  const size_t budget = P.staged ? std::min<size_t>(24 * 1024, kSmemMax - regions_max)
+                                 : kSmemBudget;
+  size_t scratch_max = 0;
   int a = 0;
   for (int j = 0; j < nl; ++j) {
     const LoopDesc &L = cv.loops[j];
-    LoopPlan &P = plan->loops[j];
-    DLoop &D = plan->host_loops[j];
+    LoopPlan &LP = P.loops[j];
+    DLoop &D = P.host_loops[j];
     fill_dloop(D, cv, j, args + a, ctx, use_local);
     int spp = 0;
     for (int d = 0; d < D.n_desc; ++d) {
       if (L.desc[d].map < 0 || L.desc[d].mode == LT_READ) continue;
       D.a[d].inc_off = spp;  // scaled by chunk below
       spp += D.a[d].arity * D.a[d].vpe;
-      P.inc_desc.push_back(d);
+      LP.inc_desc.push_back(d);
     }
-    P.scratch_per_pos = spp;
-    P.chunk = choose_chunk(spp, kSmemBudget);
-    for (int d : P.inc_desc) D.a[d].inc_off *= P.chunk;
-    plan->smem_bytes = std::max(plan->smem_bytes, sizeof(double) * (size_t)spp * P.chunk);
-    D.chunk = P.chunk;
-    D.offsets = s->lists[j].offsets.get();
-    D.elements = s->lists[j].elements.get();
-    if (use_local) {
+    LP.scratch_per_pos = spp;
+    LP.chunk = choose_chunk(spp, budget, block);
+    for (int d : LP.inc_desc) D.a[d].inc_off *= LP.chunk;
+    scratch_max = std::max(scratch_max, sizeof(double) * (size_t)spp * LP.chunk);
+    D.chunk = LP.chunk;
+    const LoopLists &Lj = s->lists[j];
+    D.offsets = Lj.offsets.get();
+    D.elements = Lj.elements.get();
+    if (use_local && !P.staged) {
       for (int d = 0; d < D.n_desc; ++d) {
         if (L.desc[d].map < 0) continue;
         auto it = s->local_maps.find(std::make_pair(j, (int)L.desc[d].map));
@@ -501,36 +1468,132 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         D.a[d].lmap = it->second.get();
       }
     }
-    if (!P.inc_desc.empty()) {
+    if (P.staged) {
+      LP.slots.resize(D.n_desc);
+      for (int d = 0; d < D.n_desc; ++d) {
+        const lt_desc &X = L.desc[d];
+        const int ar = X.map < 0 ? 1 : cv.maps[X.map].arity;
+        const int space = X.map < 0 ? L.space : cv.maps[X.map].target;
+        const Footprint &fp = P.fp.at(space);
+        LP.slots[d].alloc(std::max<int64_t>(Lj.n * ar, 1), ctx.stream);
+        if (Lj.n)
+          k_slots<<<grid_for(Lj.n * ar, 256), 256, 0, ctx.stream>>>(
+              Lj.elements.get(), Lj.sigma.get(), X.map < 0 ? nullptr : cv.maps[X.map].values, ar,
+              Lj.n, P.region.get(), fp.off.get(), fp.elem.get(), LP.slots[d].get());
+        LT_CK_LAUNCH();
+        D.a[d].slot = LP.slots[d].get();
+        D.a[d].ds = ds_of[a + d];
+      }
+    }
+    if (!LP.inc_desc.empty()) {
       std::vector<int32_t> off(s->n_tiles + 1);
-      LT_CK(cudaMemcpyAsync(off.data(), s->lists[j].offsets.get(),
-                            sizeof(int32_t) * (s->n_tiles + 1), cudaMemcpyDeviceToHost,
-                            ctx.stream));
+      LT_CK(cudaMemcpyAsync(off.data(), Lj.offsets.get(), sizeof(int32_t) * (s->n_tiles + 1),
+                            cudaMemcpyDeviceToHost, ctx.stream));
       LT_CK(cudaStreamSynchronize(ctx.stream));
       std::vector<int32_t> cb(s->n_tiles + 1, 0);
       for (int t = 0; t < s->n_tiles; ++t)
-        cb[t + 1] = cb[t] + (off[t + 1] - off[t] + P.chunk - 1) / P.chunk;
-      P.chunk_base.alloc(s->n_tiles + 1, ctx.stream);
-      LT_CK(cudaMemcpyAsync(P.chunk_base.get(), cb.data(), sizeof(int32_t) * cb.size(),
+        cb[t + 1] = cb[t] + (off[t + 1] - off[t] + LP.chunk - 1) / LP.chunk;
+      LP.chunk_base.alloc(s->n_tiles + 1, ctx.stream);
+      LT_CK(cudaMemcpyAsync(LP.chunk_base.get(), cb.data(), sizeof(int32_t) * cb.size(),
                             cudaMemcpyHostToDevice, ctx.stream));
-      D.chunk_base = P.chunk_base.get();
-      P.inc.resize(P.inc_desc.size());
-      for (size_t i = 0; i < P.inc_desc.size(); ++i) {
-        const int d = P.inc_desc[i];
-        build_inc_plan(ctx, s, j, cv.maps[L.desc[d].map], P.chunk, cb, P.chunk_base, P.inc[i]);
+      if (P.staged) {
+        std::vector<int32_t> gct(std::max<int32_t>(cb.back(), 1), 0);
+        for (int t = 0; t < s->n_tiles; ++t)
+          for (int g = cb[t]; g < cb[t + 1]; ++g) gct[g] = t;
+        LP.gc_tile.alloc((int64_t)gct.size(), ctx.stream);
+        LT_CK(cudaMemcpyAsync(LP.gc_tile.get(), gct.data(), sizeof(int32_t) * gct.size(),
+                              cudaMemcpyHostToDevice, ctx.stream));
+      }
+      D.chunk_base = LP.chunk_base.get();
+      // one ordered-gather plan per distinct map (e.g. ru and rs through if2c share one)
+      for (size_t i = 0; i < LP.inc_desc.size(); ++i) {
+        const int m = L.desc[LP.inc_desc[i]].map;
+        if (std::find(LP.plan_map.begin(), LP.plan_map.end(), m) == LP.plan_map.end())
+          LP.plan_map.push_back(m);
+      }
+      LP.inc.resize(LP.plan_map.size());
+      for (size_t p = 0; p < LP.plan_map.size(); ++p) {
+        const lt_map &mp = cv.maps[LP.plan_map[p]];
+        build_inc_plan(ctx, s, j, mp, LP.chunk, cb, LP.chunk_base, LP.inc[p],
+                       P.staged ? &P.fp.at(mp.target) : nullptr,
+                       P.staged ? &LP.gc_tile : nullptr);
+      }
+      for (size_t i = 0; i < LP.inc_desc.size(); ++i) {
+        const int d = LP.inc_desc[i];
+        const int p = (int)(std::find(LP.plan_map.begin(), LP.plan_map.end(), L.desc[d].map) -
+                            LP.plan_map.begin());
         IncPlan &IP = D.inc[i];
         IP.desc = d;
-        IP.gc_off = P.inc[i].gc_off.get();
-        IP.utgt = P.inc[i].utgt.get();
-        IP.ut_off = P.inc[i].ut_off.get();
-        IP.slots = P.inc[i].slots.get();
+        IP.plan = p;
+        IP.gc_off = LP.inc[p].gc_off.get();
+        IP.utgt = LP.inc[p].utgt.get();
+        IP.ut_off = LP.inc[p].ut_off.get();
+        IP.slots = LP.inc[p].slots.get();
       }
-      D.n_inc = (int)P.inc_desc.size();
+      D.n_inc = (int)LP.inc_desc.size();
     }
     a += D.n_desc;
   }
-  plan->dloops.alloc(nl, ctx.stream);
-  LT_CK(cudaMemcpyAsync(plan->dloops.get(), plan->host_loops.data(), sizeof(DLoop) * nl,
+  if (P.staged) {
+    // written flags per staged dataset; a dataset needs no load when its first
+    // access in the chain is a direct WRITE over exactly the rows it writes
+    StagedParams &H = P.sp;
+    std::memset(&H, 0, sizeof(H));
+    H.n_loops = nl;
+    H.n_ds = (int)ds_ptr.size();
+    std::map<int, int> sp_index;
+    for (auto &kv : P.fp) {
+      const int k = (int)sp_index.size();
+      sp_index[kv.first] = k;
+    }
+    H.n_sp = (int)sp_index.size();
+    P.wflags.resize(ds_ptr.size());
+    for (size_t k = 0; k < ds_ptr.size(); ++k) {
+      H.ds[k].data = ds_ptr[k];
+      H.ds[k].vpe = ds_vpe[k];
+      H.ds[k].sp = sp_index.at(ds_space[k]);
+      H.ds[k].load = 1;
+    }
+    a = 0;
+    for (int j = 0; j < nl; ++j) {
+      const LoopDesc &L = cv.loops[j];
+      const LoopLists &Lj = s->lists[j];
+      for (size_t d = 0; d < L.desc.size(); ++d) {
+        const int k = ds_of[a + d];
+        if (L.desc[d].mode == LT_READ) continue;
+        if (!P.wflags[k].get()) {
+          const Footprint &fp = P.fp.at(ds_space[k]);
+          P.wflags[k].alloc(std::max<int64_t>(fp.off_host.back(), 1), ctx.stream);
+          LT_CK(cudaMemsetAsync(P.wflags[k].get(), 0, P.wflags[k].n, ctx.stream));
+          H.ds[k].wflag = P.wflags[k].get();
+        }
+        const int ar = L.desc[d].map < 0 ? 1 : cv.maps[L.desc[d].map].arity;
+        if (Lj.n)
+          k_mark_written<<<grid_for(Lj.n * ar, 256), 256, 0, ctx.stream>>>(
+              Lj.elements.get(), Lj.sigma.get(), ar, Lj.n, P.fp.at(ds_space[k]).off.get(),
+              P.loops[j].slots[d].get(), P.wflags[k].get());
+        LT_CK_LAUNCH();
+      }
+      a += (int)L.desc.size();
+    }
+    for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
+    const size_t blob_max = build_blobs(ctx, s, cv, P, sp_index, ds_space);
+    H.blob = P.blob.get();
+    H.blob_off = P.blob_off.get();
+    H.blob_len = P.blob_len.get();
+    if (blob_max + P.data_max + scratch_max > kSmemMax) {  // caller falls back
+      g_last_fit = "tile program " + std::to_string(blob_max) + " B + rows " +
+                   std::to_string(P.data_max) + " B + scratch " + std::to_string(scratch_max) +
+                   " B > " + std::to_string(kSmemMax) + " B";
+      return nullptr;
+    }
+    P.smem_bytes = blob_max + P.data_max + scratch_max;
+    if (P.dataflow) build_dependencies(ctx, s, P);
+  } else {
+    P.smem_bytes = scratch_max;
+  }
+  P.dloops.alloc(nl, ctx.stream);
+  LT_CK(cudaMemcpyAsync(P.dloops.get(), P.host_loops.data(), sizeof(DLoop) * nl,
                         cudaMemcpyHostToDevice, ctx.stream));
   // colour phases: core tiles by ascending colour, then boundary tiles
   for (int reg : {LT_CORE, LT_BOUNDARY}) {
@@ -541,51 +1604,122 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       DevBuf<int32_t> ids((int64_t)kv.second.size(), ctx.stream);
       LT_CK(cudaMemcpyAsync(ids.get(), kv.second.data(), sizeof(int32_t) * kv.second.size(),
                             cudaMemcpyHostToDevice, ctx.stream));
-      plan->phases.emplace_back((int)kv.second.size(), std::move(ids));
-      plan->phase_region.push_back(reg);
-      plan->phase_color.push_back(kv.first);
+      P.phases.emplace_back((int)kv.second.size(), std::move(ids));
+      P.phase_region.push_back(reg);
+      P.phase_color.push_back(kv.first);
     }
   }
   LT_CK(cudaStreamSynchronize(ctx.stream));
   return plan;
 }
 
+typedef void (*StagedFn)(const StagedParams, const int32_t *);
+static StagedFn staged_fn(int fam) {
+  switch (fam) {
+    case 0: return k_staged_tiles<0>;
+    case 1: return k_staged_tiles<1>;
+    case 2: return k_staged_tiles<2>;
+    case 3: return k_staged_tiles<3>;
+    case 4: return k_staged_tiles<4>;
+    default: return k_staged_tiles<5>;
+  }
+}
+
+typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
+static DataflowFn dataflow_fn(int fam) {
+  switch (fam) {
+    case 0: return k_dataflow<0>;
+    case 1: return k_dataflow<1>;
+    case 2: return k_dataflow<2>;
+    case 3: return k_dataflow<3>;
+    case 4: return k_dataflow<4>;
+    default: return k_dataflow<5>;
+  }
+}
+
 static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_arg *args,
-                          int phases, int use_local, lt_exec_info *info) {
+                          int phases, int use_local, int repeats, lt_exec_info *info) {
   if ((int)cv.loops.size() != s->n_loops)
     fail(LT_E_STALE_SCHEDULE, "schedule loop count differs from chain");
   for (int j = 0; j < s->n_loops; ++j)
     if (s->loop_space[j] != cv.loops[j].space || s->lists[j].n != cv.total(cv.loops[j].space))
       fail(LT_E_STALE_SCHEDULE, "schedule was inspected for a different chain");
+  if (repeats < 1) fail(LT_E_VALUE, "repeats must be >= 1");
+  if (repeats > 1 && phases != (LT_PHASE_CORE | LT_PHASE_BOUNDARY))
+    fail(LT_E_VALUE, "repeated execution needs both phases (no halo exchange in between)");
   validate_bindings(ctx, cv, args);
-  const std::string key = plan_key(cv, args, use_local);
+  const std::string key = plan_key(cv, args, use_local) + std::to_string(exec_preference());
   if (!s->plan || s->plan->key != key) {
     s->plan = build_plan(ctx, s, cv, args, use_local);
+    if (!s->plan) {  // tile programs do not fit shared memory
+      if (exec_preference() > 0)
+        fail(LT_E_EXECUTION, "LT_EXEC=staged/dataflow: " + g_last_fit);
+      s->plan = build_plan(ctx, s, cv, args, use_local, true);
+    }
     s->plan->key = key;
   }
   ExecPlan &P = *s->plan;
-  FusedFn fn = fused_fn(chain_family(cv));
+  const int fam = chain_family(cv);
+  const void *fn = P.dataflow  ? (const void *)dataflow_fn(fam)
+                   : P.staged ? (const void *)staged_fn(fam)
+                              : (const void *)fused_fn(fam);
   if (P.smem_bytes > 48 * 1024)
-    LT_CK(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LT_CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)P.smem_bytes));
   int launches = 0, colors = 0;
   int64_t visits = 0;
-  for (size_t ph = 0; ph < P.phases.size(); ++ph) {
-    const int reg = P.phase_region[ph];
-    if (!((reg == LT_CORE && (phases & LT_PHASE_CORE)) ||
-          (reg == LT_BOUNDARY && (phases & LT_PHASE_BOUNDARY))))
-      continue;
-    fn<<<P.phases[ph].first, LT_BLOCK, P.smem_bytes, ctx.stream>>>(
-        P.dloops.get(), s->n_loops, P.phases[ph].second.get());
-    LT_CK_LAUNCH();
-    ++launches;
-    ++colors;
+  if (P.dataflow) {
+    if (P.grid == 0) {
+      int per_sm = 0, sms = 0;
+      LT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LT_SBLOCK, P.smem_bytes));
+      LT_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
+      P.grid = std::max(1, per_sm) * sms;
+    }
+    const bool core = phases & LT_PHASE_CORE, bnd = phases & LT_PHASE_BOUNDARY;
+    DataflowArgs D;
+    D.order = core && bnd ? P.order_all.get() : core ? P.order_core.get() : P.order_bnd.get();
+    D.n_exec = core && bnd ? P.n_all : core ? P.n_core : P.n_bnd;
+    D.n_items = D.n_exec * repeats;
+    D.nbr_off = P.nbr_off.get();
+    D.nbr = P.nbr.get();
+    D.done = P.done.get();
+    D.queue = P.queue.get();
+    if (core)  // a boundary-only call continues the counters of its core call
+      LT_CK(cudaMemsetAsync(P.done.get(), 0, 4 * P.done.n, ctx.stream));
+    LT_CK(cudaMemsetAsync(P.queue.get(), 0, 4, ctx.stream));
+    if (D.n_items > 0) {
+      dataflow_fn(fam)<<<std::min(P.grid, D.n_items), LT_SBLOCK, P.smem_bytes, ctx.stream>>>(P.sp,
+                                                                                         D);
+      LT_CK_LAUNCH();
+      ++launches;
+    }
+    colors = (int)P.phases.size();
+  } else {
+    for (int r = 0; r < repeats; ++r) {
+      for (size_t ph = 0; ph < P.phases.size(); ++ph) {
+        const int reg = P.phase_region[ph];
+        if (!((reg == LT_CORE && (phases & LT_PHASE_CORE)) ||
+              (reg == LT_BOUNDARY && (phases & LT_PHASE_BOUNDARY))))
+          continue;
+        if (P.staged)
+          staged_fn(fam)<<<P.phases[ph].first, LT_SBLOCK, P.smem_bytes, ctx.stream>>>(
+              P.sp, P.phases[ph].second.get());
+        else
+          fused_fn(fam)<<<P.phases[ph].first, LT_BLOCK, P.smem_bytes, ctx.stream>>>(
+              P.dloops.get(), s->n_loops, P.phases[ph].second.get());
+        LT_CK_LAUNCH();
+        ++launches;
+        if (r == 0) ++colors;
+      }
+    }
   }
-  for (int j = 0; j < s->n_loops; ++j) visits += cv.exec_size(cv.loops[j].space);
+  for (int j = 0; j < s->n_loops; ++j) visits += cv.exec_size(cv.loops[j].space) * repeats;
   if (info) {
     info->launches = launches;
     info->n_colors = colors;
     info->elements = visits;
+    info->staged = P.dataflow ? 2 : P.staged ? 1 : 0;
+    info->smem_bytes = (int32_t)P.smem_bytes;
   }
 }
 
@@ -711,7 +1845,18 @@ extern "C" int lt_execute(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain, co
   LT_API_BEGIN
   if (!ctx || !s || !chain || !args) fail(LT_E_VALUE, "null argument");
   ChainView cv(chain);
-  execute_tiled(*ctx, s, cv, args, phases, use_local_maps ? 1 : 0, info);
+  execute_tiled(*ctx, s, cv, args, phases, use_local_maps ? 1 : 0, 1, info);
+  LT_API_END
+}
+
+extern "C" int lt_execute_repeat(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain,
+                                 const lt_arg *args, int32_t repeats, int32_t use_local_maps,
+                                 lt_exec_info *info) {
+  LT_API_BEGIN
+  if (!ctx || !s || !chain || !args) fail(LT_E_VALUE, "null argument");
+  ChainView cv(chain);
+  execute_tiled(*ctx, s, cv, args, LT_PHASE_CORE | LT_PHASE_BOUNDARY, use_local_maps ? 1 : 0,
+                repeats, info);
   LT_API_END
 }
 

@@ -45,11 +45,31 @@ struct DArg {
   int32_t vpe;
   int32_t mode;
   int32_t inc_off;      // tiled: offset (doubles) of this descriptor's slots in smem
+  const int32_t *slot;  // staged: footprint slot per list position (direct) or (position, k)
+  int32_t ds;           // staged: index of the staged dataset this descriptor binds
+  int32_t pad;
+};
+
+#define LT_MAX_STAGED 16  // distinct datasets staged in shared memory
+#define LT_SBLOCK 128     // threads per CTA of the staged tile executor
+
+// One dataset staged in shared memory: the tile's footprint rows of it are
+// gathered at tile start and the rows the tile wrote are stored back at the end.
+#define LT_MAX_SPACES 8   // spaces with a staged footprint
+#define LT_MAX_SLOOPS 24  // loops of a chain run by the staged executor
+
+struct StageDS {
+  double *data;
+  const uint8_t *wflag;    // per footprint entry: written by the tile (nullptr: read-only)
+  int32_t vpe;
+  int32_t sp;              // footprint space index
+  int32_t load;            // 0: every footprint row is written before it is read
+  int32_t pad;
 };
 
 struct IncPlan {
   int32_t desc;
-  int32_t pad;
+  int32_t plan;           // staged: index of the (loop, map) apply plan in the tile program
   const int32_t *gc_off;  // per global chunk: range of unique targets
   const int32_t *utgt;    // unique target ids
   const int32_t *ut_off;  // per unique target: range of contributor slots

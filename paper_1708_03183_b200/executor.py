@@ -319,7 +319,7 @@ class TiledRunner:
     """
 
     def __init__(self, schedule, chain: LoopChain, bindings, datasets: dict,
-                 registry: KernelRegistry, use_local_maps: bool = True):
+                 registry: KernelRegistry, use_local_maps: bool = True, repeats: int = 1):
         from . import _lib
         if schedule.fingerprint != chain.fingerprint:
             raise StaleScheduleError("schedule was inspected for a different chain")
@@ -328,13 +328,20 @@ class TiledRunner:
         self.bound = _bind(chain, bindings, datasets, registry)
         self.handle = schedule.device_handle(chain)
         self.use_local_maps = use_local_maps
+        self.repeats = repeats
         info = self()  # builds the execution plan outside any capture
         self.launches_per_call = info.launches
+        self.executor = {0: "global", 1: "staged", 2: "dataflow"}[info.staged]
+        self.smem_bytes = info.smem_bytes
 
     def __call__(self):
-        return self._lib.execute(self.handle, self.bound.desc, self.bound.args,
-                                 self._lib.PHASE_CORE | self._lib.PHASE_BOUNDARY,
-                                 self.use_local_maps)
+        """Execute the chain ``repeats`` times (one persistent launch when dataflow)."""
+        if self.repeats == 1:
+            return self._lib.execute(self.handle, self.bound.desc, self.bound.args,
+                                     self._lib.PHASE_CORE | self._lib.PHASE_BOUNDARY,
+                                     self.use_local_maps)
+        return self._lib.execute_repeat(self.handle, self.bound.desc, self.bound.args,
+                                        self.repeats, self.use_local_maps)
 
     def graph(self, repeats: int = 1):
         """CUDA graph replaying ``repeats`` chain executions back to back."""

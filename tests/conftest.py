@@ -55,3 +55,10 @@ def parse_case(name: str):
 @pytest.fixture(scope="session")
 def golden():
     return golden_schedules()
+
+
+@pytest.fixture(params=["dataflow", "staged", "global"])
+def exec_mode(request, monkeypatch):
+    """Run a GPU executor test with shared-memory staging and with the global path."""
+    monkeypatch.setenv("LT_EXEC", request.param)
+    return request.param

@@ -9,7 +9,7 @@ from cases import dg_setup
 import paper_1708_03183_b200 as lt
 from paper_1708_03183_b200.dg import ElasticProblem, elastic_problem
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("exec_mode")]
 DG_CASES = sorted(c for c in golden_schedules()["schedules"] if c.startswith("dg"))
 MODES = {"sequential": lt.ExecMode.SEQUENTIAL, "shared": lt.ExecMode.SHARED}
 RTOL = 1e-12  # north_star: float64 fields within 1e-12 relative (normwise per field)
@@ -52,7 +52,7 @@ def test_gpu_dg_tiled_equals_untiled_at_scale(p, steps):
     st = elastic_setup(48, 40, p, steps, material=("uniform", 3), sigma=6.0)
     a = elastic_problem(st)
     a.run_untiled(n_chains=2)
-    for ts, mode in ((64, lt.ExecMode.SHARED), (256, lt.ExecMode.SHARED)):
+    for ts, mode in ((32, lt.ExecMode.SHARED), (128 // (p * steps), lt.ExecMode.SHARED)):
         st2 = elastic_setup(48, 40, p, steps, material=("uniform", 3), sigma=6.0)
         b = elastic_problem(st2)
         b.run_tiled(lt.inspect_chain(b.chain, ts, mode), n_chains=2)
@@ -69,3 +69,20 @@ def test_gpu_dg_p4_matches_oracle():
     pb.run_tiled(lt.inspect_chain(pb.chain, 8, lt.ExecMode.SHARED))
     for n in ("u", "s", "ru", "rs"):
         assert rel_err(pb.datasets[n].numpy(), data[n]) <= RTOL, n
+
+
+@pytest.mark.parametrize("repeats", [1, 3])
+def test_gpu_dg_repeat_equals_sequential_calls(repeats):
+    from paper_1708_03183_b200.dg import elastic_setup
+    from paper_1708_03183_b200.executor import TiledRunner
+    st = elastic_setup(40, 30, 1, 1, sigma=5.0)
+    a = elastic_problem(st)
+    a.install_params()
+    s = lt.inspect_chain(a.chain, 24, lt.ExecMode.SHARED)
+    for _ in range(repeats):
+        lt.execute_schedule(s, a.chain, a.bindings, a.datasets, a.registry, use_local_maps=True)
+    b = elastic_problem(elastic_setup(40, 30, 1, 1, sigma=5.0))
+    s2 = lt.inspect_chain(b.chain, 24, lt.ExecMode.SHARED)
+    TiledRunner(s2, b.chain, b.bindings, b.datasets, b.registry, repeats=repeats)
+    for n in ("u", "s", "ru", "rs"):
+        np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
