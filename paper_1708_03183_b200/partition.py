@@ -1,0 +1,296 @@
+"""Split a mesh into per-rank local meshes with extended halos of a given depth.
+
+Same decomposition as the reference (``pkg/src/looptile/partition.py:85-241``),
+restated with vectorised numpy so it reaches the 67M-cell configuration:
+
+* ownership by contiguous cell blocks (``np.array_split``); a vertex / edge
+  belongs to the lowest rank among its incident / flanking cells;
+* ``depth`` strips of off-rank cells grown through shared vertices: strips
+  1..depth-1 are executable halo (exec), strip ``depth`` is non-exec;
+* per space, elements ordered core | owned | exec | non-exec, each by global
+  id; an owned element is "core" iff every cell around it (through its
+  vertices) is owned by the rank;
+* symmetric exchange tables per (space, neighbour), ordered by global id.
+
+Parity: ``tests/test_partition.py`` checks sizes, global ids, local maps and
+exchange tables against the reference's output (``tests/golden``).
+
+Additions for the B200 path: ``LocalMesh.cell_edges()`` (local c2e) and
+``LocalMesh.facets()`` (interior/exterior facet spaces with local if2c/ef2c,
+split by the *global* flank count, missing flanks sent to the present cell;
+SURVEY section 7 "Local f2c maps at partition edges").
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .chain import IterationSpace, MeshMap
+from .errors import PartitionBugError
+from .mesh import CELLS, EDGES, VERTS, Mesh, cell_edge_map
+
+_REGION_CODES = {"core": 0, "owned": 1, "exec": 2, "nonexec": 3}
+
+
+@dataclass(frozen=True)
+class RegionSizes:
+    core: int
+    owned: int
+    exec: int
+    nonexec: int
+
+    @property
+    def total(self) -> int:
+        return self.core + self.owned + self.exec + self.nonexec
+
+    @property
+    def owned_total(self) -> int:
+        return self.core + self.owned
+
+
+@dataclass(frozen=True, eq=False)
+class LocalMesh:
+    """One rank's view: renumbered locally, regions contiguous (``partition.py:40-73``)."""
+
+    rank: int
+    sizes: dict
+    cells_to_vertices: np.ndarray
+    edges_to_vertices: np.ndarray
+    vertex_coords: np.ndarray
+    global_ids: dict
+    exchange_table: dict
+    global_c2e: np.ndarray | None = None   # global c2e (for local facets)
+    global_flanks: np.ndarray | None = None  # (E, 2) global flank cells, -1 missing
+
+    def neighbors(self) -> list[int]:
+        return sorted({nbr for (_, nbr) in self.exchange_table})
+
+    def spaces(self) -> dict[str, IterationSpace]:
+        return {name: IterationSpace(name, s.core, s.owned + s.exec, s.nonexec)
+                for name, s in self.sizes.items()}
+
+    def maps(self, spaces: dict | None = None) -> dict[str, MeshMap]:
+        spaces = spaces or self.spaces()
+        return {
+            "c2v": MeshMap("c2v", spaces[CELLS], spaces[VERTS], 3, self.cells_to_vertices),
+            "e2v": MeshMap("e2v", spaces[EDGES], spaces[VERTS], 2, self.edges_to_vertices),
+        }
+
+    def local_of(self, space: str) -> np.ndarray:
+        g = self.global_ids[space]
+        n = int(g.max()) + 1 if len(g) else 0
+        loc = np.full(n, -1, dtype=np.int64)
+        loc[g] = np.arange(len(g))
+        return loc
+
+    def cell_edges(self) -> np.ndarray:
+        """Local c2e: every local cell's sides are local edges (their flank is local)."""
+        loc_e = self.local_of(EDGES)
+        rows = self.global_c2e.reshape(-1, 3)[self.global_ids[CELLS]]
+        if np.any(rows >= len(loc_e)) or np.any(loc_e[rows] < 0):
+            raise PartitionBugError("a local cell has a side outside the local edge set")
+        return loc_e[rows].ravel()
+
+    def facets(self):
+        """Local interior/exterior facets (in local edge order) and their flank maps.
+
+        Returns (if_edges, if2c, ef_edges, ef2c, if_sizes, ef_sizes): local edge
+        ids of each facet space, flat local flank maps, and per-space
+        (core, boundary, nonexec) sizes following the edges' regions.
+        """
+        egid = self.global_ids[EDGES]
+        flanks = self.global_flanks[egid]                 # (E_local, 2) global cells
+        interior = flanks[:, 1] >= 0
+        loc_c = self.local_of(CELLS)
+
+        def local_cells(g):
+            out = np.full(g.shape, -1, dtype=np.int64)
+            ok = (g >= 0) & (g < len(loc_c))
+            out[ok] = loc_c[g[ok]]
+            return out
+
+        lf = local_cells(flanks)
+        # a missing flank (outside the halo) points to the present cell; such
+        # facets only occur in the non-exec strip and never execute
+        lf[:, 0] = np.where(lf[:, 0] < 0, lf[:, 1], lf[:, 0])
+        lf[:, 1] = np.where(lf[:, 1] < 0, lf[:, 0], lf[:, 1])
+        if np.any(lf < 0):
+            raise PartitionBugError("a local edge has no local flanking cell")
+        s = self.sizes[EDGES]
+        bounds = np.cumsum([0, s.core, s.owned + s.exec, s.nonexec])
+        region = np.searchsorted(bounds[1:], np.arange(len(egid)), side="right")
+        out = []
+        for mask in (interior, ~interior):
+            ids = np.flatnonzero(mask)
+            reg = region[ids]
+            sizes = (int(np.sum(reg == 0)), int(np.sum(reg == 1)), int(np.sum(reg == 2)))
+            out.append((ids, sizes))
+        (iid, isz), (eid, esz) = out
+        if2c = lf[iid].ravel()
+        ef2c = lf[eid, 0]
+        nonexec_exec = lf[iid][:sum(isz[:2])]
+        if len(nonexec_exec) and np.any(nonexec_exec < 0):
+            raise PartitionBugError("executable facet with a missing flank")
+        return iid, if2c, eid, ef2c, isz, esz
+
+
+def _incidence(tri: np.ndarray, nv: int) -> tuple[np.ndarray, np.ndarray]:
+    """Vertex -> incident cells (CSR, ascending cells)."""
+    flat = tri.ravel()
+    cells = np.repeat(np.arange(len(tri), dtype=np.int64), 3)
+    order = np.lexsort((cells, flat))
+    off = np.zeros(nv + 1, dtype=np.int64)
+    np.cumsum(np.bincount(flat, minlength=nv), out=off[1:])
+    return off, cells[order]
+
+
+def _edge_flanks(mesh: Mesh, c2e: np.ndarray) -> np.ndarray:
+    """(E, 2) flanking cells per edge, ascending, -1 for a missing second flank."""
+    cells = np.repeat(np.arange(mesh.num_cells, dtype=np.int64), 3)
+    order = np.lexsort((cells, c2e))
+    counts = np.bincount(c2e, minlength=mesh.num_edges)
+    first = np.zeros(mesh.num_edges + 1, dtype=np.int64)
+    np.cumsum(counts, out=first[1:])
+    fl = np.full((mesh.num_edges, 2), -1, dtype=np.int64)
+    fl[:, 0] = cells[order[first[:-1]]]
+    two = counts == 2
+    fl[two, 1] = cells[order[first[:-1][two] + 1]]
+    return fl
+
+
+def _segment_reduce(values: np.ndarray, off: np.ndarray, op) -> np.ndarray:
+    return op.reduceat(values, off[:-1]) if len(values) else np.zeros(len(off) - 1, np.int64)
+
+
+def partition_for_ranks(mesh: Mesh, nranks: int, depth: int) -> list[LocalMesh]:
+    """Reference ``partition.py:85-138`` (vectorised; same output)."""
+    if nranks < 1:
+        raise ValueError(f"nranks must be >= 1, got {nranks}")
+    if depth < 1:
+        raise ValueError(f"depth must be >= 1, got {depth}")
+    if nranks > mesh.num_cells:
+        raise ValueError(f"{nranks} ranks for {mesh.num_cells} cells")
+    C, V, E = mesh.num_cells, mesh.num_vertices, mesh.num_edges
+    tri = mesh.cells_to_vertices.reshape(-1, 3)
+    pairs = mesh.edges_to_vertices.reshape(-1, 2)
+    vc_off, vc_cells = _incidence(tri, V)
+    c2e = cell_edge_map(mesh)
+    flanks = _edge_flanks(mesh, c2e)
+
+    cell_owner = np.empty(C, dtype=np.int64)
+    for r, block in enumerate(np.array_split(np.arange(C), nranks)):
+        cell_owner[block] = r
+    inc_owner = cell_owner[vc_cells]
+    vmin = _segment_reduce(inc_owner, vc_off, np.minimum)
+    vmax = _segment_reduce(inc_owner, vc_off, np.maximum)
+    vertex_owner = vmin
+    fo = np.where(flanks >= 0, cell_owner[np.maximum(flanks, 0)], np.iinfo(np.int64).max)
+    edge_owner = fo.min(axis=1)
+    # ring owners: all cells around the entity's vertices
+    cell_rmin, cell_rmax = vmin[tri].min(axis=1), vmax[tri].max(axis=1)
+    edge_rmin, edge_rmax = vmin[pairs].min(axis=1), vmax[pairs].max(axis=1)
+
+    infos = []
+    for r in range(nranks):
+        infos.append(_build_rank(r, depth, tri, pairs, vc_off, vc_cells, flanks, cell_owner,
+                                 vertex_owner, edge_owner, (cell_rmin, cell_rmax),
+                                 (edge_rmin, edge_rmax), (vmin, vmax), mesh))
+    _fill_exchange_tables(infos, nranks, {CELLS: cell_owner, EDGES: edge_owner,
+                                          VERTS: vertex_owner})
+    return [LocalMesh(rank=i["rank"], sizes=i["sizes"], cells_to_vertices=i["c2v"],
+                      edges_to_vertices=i["e2v"], vertex_coords=i["coords"],
+                      global_ids=i["gids"], exchange_table=i["exchange"],
+                      global_c2e=c2e, global_flanks=flanks) for i in infos]
+
+
+def _build_rank(r, depth, tri, pairs, vc_off, vc_cells, flanks, cell_owner, vertex_owner,
+                edge_owner, cring, ering, vring, mesh) -> dict:
+    C = len(tri)
+    strip = np.full(C, -1, dtype=np.int64)
+    owned = cell_owner == r
+    strip[owned] = 0
+    # grow strips through shared vertices; only owned cells with a foreign
+    # neighbour can reach off-rank cells
+    frontier = np.flatnonzero(owned & ((cring[0] != r) | (cring[1] != r)))
+    for k in range(1, depth + 1):
+        if not len(frontier):
+            break
+        verts = np.unique(tri[frontier].ravel())
+        cand = np.unique(vc_cells[_ranges(vc_off[verts], vc_off[verts + 1])])
+        new = cand[strip[cand] < 0]
+        strip[new] = k
+        frontier = new
+    local_cells = np.flatnonzero(strip >= 0)
+    # vertices / edges touched by local cells; strip = min over local incident cells
+    vs = np.full(len(vertex_owner), np.iinfo(np.int64).max, dtype=np.int64)
+    np.minimum.at(vs, tri[local_cells].ravel(), np.repeat(strip[local_cells], 3))
+    local_verts = np.flatnonzero(vs != np.iinfo(np.int64).max)
+    fs = np.where(flanks >= 0, strip[np.maximum(flanks, 0)], -1)
+    fs = np.where(fs < 0, np.iinfo(np.int64).max, fs)
+    es = fs.min(axis=1)
+    local_edges = np.flatnonzero(es != np.iinfo(np.int64).max)
+
+    def order(gids, owner, strp, rmin, rmax):
+        own = owner[gids] == r
+        core = own & (rmin[gids] == r) & (rmax[gids] == r)
+        code = np.where(own, np.where(core, 0, 1), np.where(strp <= depth - 1, 2, 3))
+        o = np.lexsort((gids, code))
+        g = gids[o]
+        c = code[o]
+        sizes = RegionSizes(*(int(np.sum(c == i)) for i in range(4)))
+        return sizes, g
+
+    csz, cg = order(local_cells, cell_owner, strip[local_cells], *cring)
+    vsz, vg = order(local_verts, vertex_owner, vs[local_verts], *vring)
+    esz, eg = order(local_edges, edge_owner, es[local_edges], *ering)
+    vloc = np.full(len(vertex_owner), -1, dtype=np.int64)
+    vloc[vg] = np.arange(len(vg))
+    return {
+        "rank": r,
+        "sizes": {CELLS: csz, EDGES: esz, VERTS: vsz},
+        "c2v": vloc[tri[cg]].ravel(),
+        "e2v": vloc[pairs[eg]].ravel(),
+        "coords": mesh.vertex_coords[vg],
+        "gids": {CELLS: cg, EDGES: eg, VERTS: vg},
+        "exchange": {},
+    }
+
+
+def _ranges(lo: np.ndarray, hi: np.ndarray) -> np.ndarray:
+    """Concatenation of arange(lo[i], hi[i]) (vectorised)."""
+    n = hi - lo
+    total = int(n.sum())
+    if total == 0:
+        return np.zeros(0, dtype=np.int64)
+    starts = np.repeat(lo - np.concatenate([[0], np.cumsum(n)[:-1]]), n)
+    return starts + np.arange(total)
+
+
+def _fill_exchange_tables(infos: list[dict], nranks: int, owners: dict) -> None:
+    """Pair every halo copy with its owner, ordered by global id on both sides
+    (reference ``partition.py:212-241``)."""
+    for space, owner in owners.items():
+        local = []
+        for info in infos:
+            g = info["gids"][space]
+            loc = np.full(len(owner), -1, dtype=np.int64)
+            loc[g] = np.arange(len(g))
+            local.append(loc)
+        halo = [info["gids"][space][owner[info["gids"][space]] != info["rank"]] for info in infos]
+        for r in range(nranks):
+            for s in range(nranks):
+                if s == r:
+                    continue
+                a = halo[r][owner[halo[r]] == s]          # r holds a copy of s's element
+                b = halo[s][owner[halo[s]] == r]          # s holds a copy of r's element
+                gids = np.union1d(a, b)
+                if not len(gids):
+                    continue
+                if np.any(local[s][gids] < 0) or np.any(local[r][gids] < 0):
+                    missing = gids[(local[s][gids] < 0) | (local[r][gids] < 0)][0]
+                    raise PartitionBugError(
+                        f"{space} {int(missing)} missing on rank {s} but shared with {r}")
+                infos[r]["exchange"][(space, s)] = np.stack(
+                    [local[r][gids], local[s][gids]], axis=1)

@@ -239,22 +239,32 @@ def main():
 
     # distributed: partition tables + gathered values
     dist = {}
-    mesh = L.rcm_renumber(L.generate_rect_mesh(8, 4))
-    for nranks, depth in ((2, 3), (4, 3)):
+    for tag, dims, ren, nranks, depth in (("fig2_8x4_rcm", (8, 4), "rcm", 2, 3),
+                                          ("fig2_8x4_rcm", (8, 4), "rcm", 4, 3),
+                                          ("p_16x8_none", (16, 8), "none", 3, 2),
+                                          ("p_12x10_rcm", (12, 10), "rcm", 4, 5),
+                                          ("p_16x8_rcm", (16, 8), "rcm", 8, 2),
+                                          ("p_9x7_none", (9, 7), "none", 5, 1)):
+        mesh = L.generate_rect_mesh(*dims)
+        if ren == "rcm":
+            mesh = L.rcm_renumber(mesh)
         lms = L.partition_for_ranks(mesh, nranks, depth)
+        pre = f"{tag}/n{nranks}"
+        dist[f"{pre}/depth"] = np.array([depth])
         for lm in lms:
             for space, sz in lm.sizes.items():
-                key = f"fig2_8x4_rcm/n{nranks}/r{lm.rank}/{space}"
+                key = f"{pre}/r{lm.rank}/{space}"
                 dist[key + "/sizes"] = np.array([sz.core, sz.owned, sz.exec, sz.nonexec])
                 dist[key + "/gids"] = lm.global_ids[space]
-            dist[f"fig2_8x4_rcm/n{nranks}/r{lm.rank}/c2v"] = lm.cells_to_vertices
-            dist[f"fig2_8x4_rcm/n{nranks}/r{lm.rank}/e2v"] = lm.edges_to_vertices
+            dist[f"{pre}/r{lm.rank}/c2v"] = lm.cells_to_vertices
+            dist[f"{pre}/r{lm.rank}/e2v"] = lm.edges_to_vertices
             for (space, nbr), table in lm.exchange_table.items():
-                dist[f"fig2_8x4_rcm/n{nranks}/r{lm.rank}/x/{space}/{nbr}"] = table
-        res = L.run_distributed(mesh, L.PRESETS["fig2"], nranks, 4, depth=depth, registry=reg,
-                                poison_halo=True)
-        for n, v in res.datasets.items():
-            dist[f"fig2_8x4_rcm/n{nranks}/gathered/{n}"] = v
+                dist[f"{pre}/r{lm.rank}/x/{space}/{nbr}"] = table
+        if tag.startswith("fig2"):
+            res = L.run_distributed(mesh, L.PRESETS["fig2"], nranks, 4, depth=depth,
+                                    registry=reg, poison_halo=True)
+            for n, v in res.datasets.items():
+                dist[f"{pre}/gathered/{n}"] = v
 
     with gzip.open(os.path.join(HERE, "schedules.json.gz"), "wt") as fh:
         json.dump({"schedules": schedules, "meta": meta, "fingerprints": fingerprints}, fh)
