@@ -64,10 +64,8 @@ def bodies(p: int, dt: float) -> dict:
         fa, fb = int(fa), int(fb)
         ta = traces(fa, u[0], s[0])
         tb = traces(fb, u[1], s[1])[:, ::-1]  # neighbour points in reversed order
-        ra, la, ma = mat[0]
-        rb, lb, mb = mat[1]
-        zpa, zsa = np.sqrt(ra * (la + 2 * ma)), np.sqrt(ra * ma)
-        zpb, zsb = np.sqrt(rb * (lb + 2 * mb)), np.sqrt(rb * mb)
+        ra, la, ma, zpa, zsa = mat[0]
+        rb, lb, mb, zpb, zsb = mat[1]
         tnx, tny = -ny, nx
         vxa, vya, sxxa, syya, sxya = ta
         vxb, vyb, sxxb, syyb, sxyb = tb
@@ -96,8 +94,7 @@ def bodies(p: int, dt: float) -> dict:
         nx, ny, jf, fa, _ = fgeo
         fa = int(fa)
         vx, vy, sxx, syy, sxy = traces(fa, u[0], s[0])
-        rho, lam, mu = mat[0]
-        zp, zs = np.sqrt(rho * (lam + 2 * mu)), np.sqrt(rho * mu)
+        rho, lam, mu, zp, zs = mat[0]
         tnx, tny = -ny, nx
         Tx, Ty = sxx * nx + sxy * ny, sxy * nx + syy * ny
         dvn = -(Tx * nx + Ty * ny) / zp

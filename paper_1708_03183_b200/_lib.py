@@ -19,7 +19,8 @@ from .errors import (ColoringLimitError, DepthExceededError, ExecutionError,
                      InspectionError, InvalidChainError, PartitionBugError,
                      StaleScheduleError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libltcuda.so")
+LIB_PATH = os.environ.get("LT_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libltcuda.so")
 
 LT_OK = 0
 _ERRORS = {

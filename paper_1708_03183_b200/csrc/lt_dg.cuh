@@ -121,8 +121,8 @@ __device__ __forceinline__ void dg_iflux(C &c) {
   dg_traces<ND, NQ>(E, fa, c.rdm(2, 0), c.rdm(3, 0), ta, false);
   dg_traces<ND, NQ>(E, fb, c.rdm(2, 1), c.rdm(3, 1), tb, true);
   const double la = ma[1], mua = ma[2], lb = mb[1], mub = mb[2];
-  const double zpa = sqrt(ma[0] * (la + 2.0 * mua)), zsa = sqrt(ma[0] * mua);
-  const double zpb = sqrt(mb[0] * (lb + 2.0 * mub)), zsb = sqrt(mb[0] * mub);
+  const double zpa = ma[3], zsa = ma[4], zpb = mb[3], zsb = mb[4];  // impedances rho*c_p, rho*c_s
+  const double ip = 1.0 / (zpa + zpb), is = 1.0 / (zsa + zsb);
   const double tnx = -ny, tny = nx;
   double ca[5][NQ], cb[5][NQ];
 #pragma unroll
@@ -133,8 +133,8 @@ __device__ __forceinline__ void dg_iflux(C &c) {
     const double vnb = tb[0][q] * nx + tb[1][q] * ny, vtb = tb[0][q] * tnx + tb[1][q] * tny;
     const double Tna = Tax * nx + Tay * ny, Tta = Tax * tnx + Tay * tny;
     const double Tnb = Tbx * nx + Tby * ny, Ttb = Tbx * tnx + Tby * tny;
-    const double dvn = (Tnb - Tna + zpb * (vnb - vna)) / (zpa + zpb);
-    const double dvt = (Ttb - Tta + zsb * (vtb - vta)) / (zsa + zsb);
+    const double dvn = (Tnb - Tna + zpb * (vnb - vna)) * ip;
+    const double dvt = (Ttb - Tta + zsb * (vtb - vta)) * is;
     const double dTax = zpa * dvn * nx + zsa * dvt * tnx;
     const double dTay = zpa * dvn * ny + zsa * dvt * tny;
     const double dvax = dvn * nx + dvt * tnx, dvay = dvn * ny + dvt * tny;
@@ -169,14 +169,14 @@ __device__ __forceinline__ void dg_eflux(C &c) {
   double t[5][NQ];
   dg_traces<ND, NQ>(E, fa, c.rdm(2, 0), c.rdm(3, 0), t, false);
   const double lam = m[1], mu = m[2];
-  const double zp = sqrt(m[0] * (lam + 2.0 * mu)), zs = sqrt(m[0] * mu);
+  const double izp = 1.0 / m[3], izs = 1.0 / m[4];
   const double tnx = -ny, tny = nx;
   double cr[5][NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const double Tx = t[2][q] * nx + t[4][q] * ny, Ty = t[4][q] * nx + t[3][q] * ny;
-    const double dvn = -(Tx * nx + Ty * ny) / zp;
-    const double dvt = -(Tx * tnx + Ty * tny) / zs;
+    const double dvn = -(Tx * nx + Ty * ny) * izp;
+    const double dvt = -(Tx * tnx + Ty * tny) * izs;
     const double dvx = dvn * nx + dvt * tnx, dvy = dvn * ny + dvt * tny;
     const double dn = dvx * nx + dvy * ny;
     cr[0][q] = -Tx;
@@ -251,8 +251,8 @@ inline int64_t dg_param_count(int k) {
 inline void dg_validate(int k, size_t j, const ChainView &cv, const LoopDesc &L,
                         const lt_arg *args) {
   const int p = k / 5 + 1, which = k % 5, nd = dg_nd(p);
-  static const int want[5][6] = {{5, 3, 2, 3, 2, 3}, {5, 3, 2, 3, 2, 3}, {5, 3, 2, 3, 2, 3},
-                                 {5, 3, 2, 3, 0, 0}, {2, 3, 2, 3, 0, 0}};
+  static const int want[5][6] = {{5, 5, 2, 3, 2, 3}, {5, 5, 2, 3, 2, 3}, {5, 5, 2, 3, 2, 3},
+                                 {5, 5, 2, 3, 0, 0}, {2, 3, 2, 3, 0, 0}};
   static const bool scaled[5][6] = {{0, 0, 1, 1, 1, 1}, {0, 0, 1, 1, 1, 1}, {0, 0, 1, 1, 1, 1},
                                     {0, 0, 1, 1, 0, 0}, {1, 1, 1, 1, 0, 0}};
   for (size_t d = 0; d < L.desc.size(); ++d) {

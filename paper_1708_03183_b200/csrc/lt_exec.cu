@@ -108,7 +108,7 @@ struct StagedCtx {
   __device__ const double *params() const { return L.params; }
   __device__ int elem() const { return e; }
   __device__ double *row(int d, int slot) const {
-    return smem + base[L.a[d].ds] + slot * L.a[d].vpe;
+    return smem + base[L.a[d].ds] + slot * L.a[d].sstride;
   }
   __device__ const double *rd(int d) const { return row(d, B[sbase[d] + pos]); }
   __device__ double *wr(int d) const { return row(d, B[sbase[d] + pos]); }
@@ -235,6 +235,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+#ifdef LT_PHASE_TIMING
+// profiling build only: per-phase cycle totals of the staged executor (thread 0)
+__device__ unsigned long long g_phase_cycles[40];
+#define LT_TSTAMP(var) long long var = clock64()
+#define LT_TACC(slot, t0)                                                  \
+  do {                                                                     \
+    if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[slot], clock64() - (t0)); \
+  } while (0)
+#else
+#define LT_TSTAMP(var)
+#define LT_TACC(slot, t0)
+#endif
+
 // Kernel parameters of the staged executor: lives in the constant bank, so the
 // per-loop descriptor fields every thread reads are uniform broadcasts.
 //
@@ -291,127 +304,164 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
       : "memory");
 }
 
-__device__ __forceinline__ void apply_plan(const DLoop &L, const IncPlan &P, const int *gc_off,
+// Apply the contributions of one chunk for every INC/WRITE descriptor that
+// shares ordered-gather plan `p` (e.g. ru and rs through if2c): one thread per
+// unique target, contributions added in (element, k) order.
+__device__ __forceinline__ void apply_item(const DLoop &L, int desc, int cc, int u,
                                            const int *utgt, const int *ut_off, const int *slots,
-                                           int c, const double *scratch, double *smem,
-                                           const int *base) {
-  const DArg &A = L.a[P.desc];
+                                           const double *scratch, double *smem, const int *base) {
+  const DArg &A = L.a[desc];
   const int vpe = A.vpe;
-  double *rows = smem + base[A.ds];
-  const int u1 = gc_off[c + 1];
-  const double *sc = scratch + A.inc_off;
-  for (int u = gc_off[c] + threadIdx.x; u < u1; u += LT_SBLOCK) {
-    double *dst = rows + utgt[u] * vpe;
-    const int s0 = ut_off[u], s1 = ut_off[u + 1];
-    if (A.mode == LT_INC) {
-      for (int cc = 0; cc < vpe; ++cc) {
-        double v = dst[cc];
-        for (int s = s0; s < s1; ++s) v = __dadd_rn(v, sc[slots[s] * vpe + cc]);
-        dst[cc] = v;
-      }
-    } else {
-      const double *src = sc + slots[s1 - 1] * vpe;
-      for (int cc = 0; cc < vpe; ++cc) dst[cc] = src[cc];
-    }
+  const int s0 = ut_off[u], s1 = ut_off[u + 1];
+  double *dst = smem + base[A.ds] + utgt[u] * A.sstride + cc;
+  const double *sc = scratch + A.inc_off + cc;
+  if (A.mode == LT_INC) {
+    double v = *dst;
+    for (int s = s0; s < s1; ++s) v = __dadd_rn(v, sc[slots[s] * vpe]);
+    *dst = v;
+  } else {
+    *dst = sc[slots[s1 - 1] * vpe];
   }
 }
 
-// Run one tile: blob (TMA) -> footprint gather (cp.async) -> every loop on
-// shared memory -> store back the rows the tile wrote.  `phase` is the parity
-// of the CTA's mbarrier for this tile.
-template <int FAM>
-__device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base,
-                                         uint64_t *bar, unsigned phase) {
+__device__ __forceinline__ void apply_plan(const DLoop &L, int p, const int *gc_off,
+                                           const int *utgt, const int *ut_off, const int *slots,
+                                           int c, const double *scratch, double *smem,
+                                           const int *base) {
+  // descriptors sharing plan p (<= LT_MAX_INC = 4) and their offsets in the
+  // concatenated component space, kept in scalars (no local memory)
+  int d0 = -1, d1 = -1, d2 = -1, d3 = -1, c1 = 0, c2 = 0, c3 = 0, vt = 0;
+#pragma unroll
+  for (int i = 0; i < LT_MAX_INC; ++i) {
+    if (i >= L.n_inc || L.inc[i].plan != p) continue;
+    const int d = L.inc[i].desc;
+    if (d0 < 0) { d0 = d; vt += L.a[d].vpe; c1 = vt; }
+    else if (d1 < 0) { d1 = d; vt += L.a[d].vpe; c2 = vt; }
+    else if (d2 < 0) { d2 = d; vt += L.a[d].vpe; c3 = vt; }
+    else { d3 = d; vt += L.a[d].vpe; }
+  }
+  if (d1 < 0) c1 = c2 = c3 = vt;
+  else if (d2 < 0) c2 = c3 = vt;
+  else if (d3 < 0) c3 = vt;
+  const int u0 = gc_off[c], nu = gc_off[c + 1] - u0;
+  // one work item per (target, component), walked incrementally (no division)
+  const int dq = LT_SBLOCK / vt, dr = LT_SBLOCK - dq * vt;
+  int q = threadIdx.x / vt, r = threadIdx.x - q * vt;
+  while (q < nu) {
+    const int desc = r < c1 ? d0 : r < c2 ? d1 : r < c3 ? d2 : d3;
+    const int cc = r - (r < c1 ? 0 : r < c2 ? c1 : r < c3 ? c2 : c3);
+    apply_item(L, desc, cc, u0 + q, utgt, ut_off, slots, scratch, smem, base);
+    q += dq;
+    r += dr;
+    if (r >= vt) { r -= vt; ++q; }
+  }
+}
+
+// Gather the (row, component)-flattened footprint rows of dataset d into its
+// odd-stride shared rows with asynchronous 8-byte copies (coalesced within rows
+// and along runs of consecutive ids).
+__device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, double *rows) {
+  const int v = S.vpe, sv = S.stride;
+  const int nrow = B[2 * S.sp];
+  const int *idx = B + B[2 * S.sp + 1];
+  const double *src = S.data;
+  const int di = LT_SBLOCK / v, dc = LT_SBLOCK - di * v;
+  int i = threadIdx.x / v, c = threadIdx.x - i * v;
+  while (i < nrow) {
+    cp_async8(rows + i * sv + c, src + (size_t)idx[i] * v + c);
+    i += di;
+    c += dc;
+    if (c >= v) { c -= v; ++i; }
+  }
+}
+
+// Phase 1 of a tile (no dependency on other tiles): tile program via TMA,
+// shared-memory layout, and the gather of datasets the chain never writes.
+__device__ __forceinline__ void tile_prefetch(const StagedParams &P, int t, double *smem,
+                                              int *base, uint64_t *bar, unsigned phase) {
   const int tid = threadIdx.x;
   int *B = reinterpret_cast<int *>(smem);
+  LT_TSTAMP(t_blob);
   if (tid == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of smem
     bulk_load(B, P.blob + P.blob_off[t], 4u * (unsigned)P.blob_len[t], bar);
   }
   mbar_wait(bar, phase);
+  LT_TACC(0, t_blob);
   if (tid == 0) {
     int acc = P.blob_len[t] / 2;  // doubles after the blob (blob_len is a multiple of 4)
     for (int d = 0; d < P.n_ds; ++d) {
       base[d] = acc;
-      acc += (B[2 * P.ds[d].sp] * P.ds[d].vpe + 1) & ~1;  // keep every region 16-byte aligned
+      acc += B[2 * P.ds[d].sp] * P.ds[d].stride;
     }
     base[P.n_ds] = acc;
   }
   __syncthreads();
-  // gather the footprint rows of every dataset (asynchronous copies, all in flight)
-  for (int d = 0; d < P.n_ds; ++d) {
-    const StageDS &S = P.ds[d];
-    if (!S.load) continue;
-    const int vpe = S.vpe;
-    const int *idx = B + B[2 * S.sp + 1];
-    const int rows = B[2 * S.sp];
-    const double *src = S.data;
-    double *dst = smem + base[d];
-    if ((vpe & 1) == 0) {  // 16-byte rows: base[] offsets are even
-      for (int i = tid; i < rows; i += LT_SBLOCK) {
-        const double *a = src + (size_t)idx[i] * vpe;
-        double *b = dst + i * vpe;
-        for (int c = 0; c < vpe; c += 2) cp_async16(b + c, a + c);
-      }
-    } else {
-      for (int i = tid; i < rows; i += LT_SBLOCK) {
-        const double *a = src + (size_t)idx[i] * vpe;
-        double *b = dst + i * vpe;
-        for (int c = 0; c < vpe; ++c) cp_async8(b + c, a + c);
-      }
-    }
-  }
+  for (int d = 0; d < P.n_ds; ++d)
+    if (P.ds[d].ro) gather_rows(P.ds[d], B, smem + base[d]);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Phase 2: gather the datasets the chain writes, run every loop on shared
+// memory, store back the rows this tile wrote.
+template <int FAM>
+__device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base) {
+  const int tid = threadIdx.x;
+  const int *B = reinterpret_cast<const int *>(smem);
+  LT_TSTAMP(t_gather);
+  for (int d = 0; d < P.n_ds; ++d)
+    if (P.ds[d].load && !P.ds[d].ro) gather_rows(P.ds[d], B, smem + base[d]);
   cp_async_wait_all();
   __syncthreads();
+  LT_TACC(1, t_gather);
   double *scratch = smem + base[P.n_ds];
   for (int j = 0; j < P.n_loops; ++j) {
     const DLoop &L = P.loops[j];
     const int *LH = B + P.loop_pos[j];
     const int n = LH[0];
     if (n == 0) continue;
+    LT_TSTAMP(t_loop);
     const int CH = L.chunk;
     for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
+      LT_TSTAMP(t_body);
       if (tid < CH && c0 + tid < n) {
         StagedCtx cx{L, 0, c0 + tid, tid, smem, scratch, base, B, LH + 2};
         dispatch<FAM>(L.kernel, cx);
       }
+      LT_TACC(32 + (j < 4 ? j : 3), t_body);
       if (L.n_inc) {
         __syncthreads();
-        for (int i = 0; i < L.n_inc; ++i) {
-          const int *pb = LH + 2 + L.n_desc + 4 * L.inc[i].plan;
-          apply_plan(L, L.inc[i], B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem,
-                     base);
+        LT_TACC(36 + (j < 2 ? j : 1), t_body);
+        for (int pl = 0; pl < L.n_plans; ++pl) {
+          const int *pb = LH + 2 + L.n_desc + 4 * pl;
+          apply_plan(L, pl, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base);
         }
       }
       __syncthreads();
     }
+    LT_TACC(8 + (j < 24 ? j : 23), t_loop);
   }
+  LT_TSTAMP(t_wb);
+  // store back the rows this tile wrote (flattened like the gather, coalesced)
   for (int d = 0; d < P.n_ds; ++d) {
     const StageDS &S = P.ds[d];
-    const int wb = B[P.ds_pos + d];
-    if (wb < 0) continue;
-    const int vpe = S.vpe;
+    if (!S.written) continue;
+    const int v = S.vpe, sv = S.stride;
+    const int nrow = B[2 * S.sp];
     const int *idx = B + B[2 * S.sp + 1];
-    const int *flag = B + wb;
-    const int rows = B[2 * S.sp];
+    const int *flag = B + B[P.ds_pos + d];
     double *dst = S.data;
-    const double *src = smem + base[d];
-    if ((vpe & 1) == 0) {
-      for (int i = tid; i < rows; i += LT_SBLOCK) {
-        if (!flag[i]) continue;
-        double2 *b = reinterpret_cast<double2 *>(dst + (size_t)idx[i] * vpe);
-        const double2 *a = reinterpret_cast<const double2 *>(src + i * vpe);
-        for (int c = 0; c < vpe / 2; ++c) b[c] = a[c];
-      }
-    } else {
-      for (int i = tid; i < rows; i += LT_SBLOCK) {
-        if (!flag[i]) continue;
-        double *b = dst + (size_t)idx[i] * vpe;
-        const double *a = src + i * vpe;
-        for (int c = 0; c < vpe; ++c) b[c] = a[c];
-      }
+    const double *rows = smem + base[d];
+    const int di = LT_SBLOCK / v, dc = LT_SBLOCK - di * v;
+    int i = tid / v, c = tid - i * v;
+    while (i < nrow) {
+      if (flag[i]) dst[(size_t)idx[i] * v + c] = rows[i * sv + c];
+      i += di;
+      c += dc;
+      if (c >= v) { c -= v; ++i; }
     }
   }
+  LT_TACC(2, t_wb);
 }
 
 // one colour phase per launch, one CTA per tile
@@ -423,7 +473,8 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_staged_tiles(const __grid_constan
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
-  run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base, &bar, 0);
+  tile_prefetch(P, tile_ids[blockIdx.x], smem, base, &bar, 0);
+  run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base);
 }
 
 // Persistent dataflow executor: CTAs pop tile instances (repeat k, tile) from a
@@ -465,7 +516,10 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     if (it >= D.n_items) return;
     const int k = it / D.n_exec;
     const int t = D.order[it - k * D.n_exec];
+    tile_prefetch(P, t, smem, base, &bar, phase);  // overlaps the dependency wait
+    phase ^= 1u;
     const int n0 = D.nbr_off[t], n1 = D.nbr_off[t + 1];
+    LT_TSTAMP(t_wait);
     for (int i = n0 + threadIdx.x; i < n1; i += LT_SBLOCK) {
       const int e = D.nbr[i];
       const int need = k + (e & 1);
@@ -474,11 +528,20 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     }
     __threadfence();  // gpu-scope fence: drop stale L1 lines before gathering
     __syncthreads();
-    run_tile<FAM>(P, t, smem, base, &bar, phase);
-    phase ^= 1u;
-    __threadfence();
+    LT_TACC(3, t_wait);
+    LT_TSTAMP(t_tile);
+    run_tile<FAM>(P, t, smem, base);
+    // release: barrier, then one cumulative gpu-scope fence + increment
+    // (the arrive pattern of CUTLASS's GenericBarrier)
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(D.done + t, 1);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(D.done + t, 1);
+    }
+    LT_TACC(4, t_tile);
+#ifdef LT_PHASE_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[5], 1ull);
+#endif
   }
 }
 
@@ -1179,6 +1242,74 @@ static void to_host(Ctx &ctx, const DevBuf<T> &d, int64_t n, std::vector<T> &h) 
   if (n) LT_CK(cudaMemcpyAsync(h.data(), d.get(), sizeof(T) * n, cudaMemcpyDeviceToHost, ctx.stream));
 }
 
+// Runs of consecutive global ids inside each tile's footprint (optionally only
+// over flagged entries): the unit of the coalesced gather / store-back.
+__global__ void k_run_marks(const int32_t *elem, const uint32_t *tile, const uint8_t *flag,
+                            int64_t n, int32_t *head, int32_t *tail) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool on = flag ? flag[i] != 0 : true;
+  const bool cont_prev = i > 0 && tile[i - 1] == tile[i] && elem[i - 1] + 1 == elem[i] &&
+                         (flag ? flag[i - 1] != 0 : true);
+  const bool cont_next = i + 1 < n && tile[i + 1] == tile[i] && elem[i] + 1 == elem[i + 1] &&
+                         (flag ? flag[i + 1] != 0 : true);
+  head[i] = on && !cont_prev;
+  tail[i] = on && !cont_next;
+}
+
+__global__ void k_run_emit(const int32_t *elem, const uint32_t *tile, const int32_t *fp_off,
+                           const int32_t *head, const int32_t *tail, const int32_t *hidx,
+                           const int32_t *tidx, int64_t n, int32_t *runs3, uint32_t *run_tile) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (head[i]) {
+    const int r = hidx[i];
+    runs3[3 * r] = (int32_t)(i - fp_off[tile[i]]);
+    runs3[3 * r + 1] = elem[i];
+    run_tile[r] = tile[i];
+    atomicAdd(&runs3[3 * r + 2], -(int32_t)i);
+  }
+  if (tail[i]) atomicAdd(&runs3[3 * tidx[i] + 2], (int32_t)i + 1);
+}
+
+struct RunSet {
+  DevBuf<int32_t> runs3;  // (tile-local first row, first global id, length) per run
+  DevBuf<int32_t> off;    // per tile: range of runs
+  std::vector<int32_t> off_host;
+};
+
+static void build_runs(Ctx &ctx, const Footprint &fp, const uint8_t *flag, int n_tiles,
+                       RunSet &out) {
+  const int64_t n = fp.n;
+  DevBuf<int32_t> head(std::max<int64_t>(n, 1), ctx.stream), tail(std::max<int64_t>(n, 1), ctx.stream),
+      hidx(std::max<int64_t>(n, 1), ctx.stream), tidx(std::max<int64_t>(n, 1), ctx.stream);
+  int64_t R = 0;
+  if (n) {
+    k_run_marks<<<grid_for(n, 256), 256, 0, ctx.stream>>>(fp.elem.get(), fp.tile.get(), flag, n,
+                                                         head.get(), tail.get());
+    LT_CK_LAUNCH();
+    exclusive_sum(ctx, head.get(), hidx.get(), n);
+    exclusive_sum(ctx, tail.get(), tidx.get(), n);
+    R = last_plus(ctx, hidx.get(), head.get(), n);
+  }
+  out.runs3.alloc(std::max<int64_t>(3 * R, 3), ctx.stream);
+  LT_CK(cudaMemsetAsync(out.runs3.get(), 0, 4 * out.runs3.n, ctx.stream));
+  DevBuf<uint32_t> rt(std::max<int64_t>(R, 1), ctx.stream);
+  if (n) {
+    k_run_emit<<<grid_for(n, 256), 256, 0, ctx.stream>>>(fp.elem.get(), fp.tile.get(),
+                                                        fp.off.get(), head.get(), tail.get(),
+                                                        hidx.get(), tidx.get(), n, out.runs3.get(),
+                                                        rt.get());
+    LT_CK_LAUNCH();
+  }
+  out.off.alloc(n_tiles + 1, ctx.stream);
+  lower_bound_u32(ctx, rt.get(), R, n_tiles, out.off.get());
+  out.off_host.resize(n_tiles + 1);
+  LT_CK(cudaMemcpyAsync(out.off_host.data(), out.off.get(), 4 * (n_tiles + 1),
+                        cudaMemcpyDeviceToHost, ctx.stream));
+  LT_CK(cudaStreamSynchronize(ctx.stream));
+}
+
 // Lay out and fill the per-tile programs; returns the largest blob in bytes.
 static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPlan &P,
                           const std::map<int, int> &sp_index, const std::vector<int> &ds_space) {
@@ -1209,6 +1340,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   LT_CK(cudaStreamSynchronize(ctx.stream));
   std::vector<const Footprint *> fps(H.n_sp);
   for (auto &kv : sp_index) fps[kv.second] = &P.fp.at(kv.first);
+
   // sections in blob order
   std::vector<Section> secs;
   auto sec = [&](const void *src, bool u8) -> Section & {
@@ -1407,11 +1539,11 @@ static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_
     size_t r = 0;
     for (size_t k = 0; k < ds_ptr.size(); ++k) {
       const auto &oh = P.fp[ds_space[k]].off_host;
-      r += (size_t)(oh[t + 1] - oh[t]) * ds_vpe[k];
+      r += (size_t)(oh[t + 1] - oh[t]) * (ds_vpe[k] | 1);
     }
     regions_max = std::max(regions_max, r * sizeof(double));
   }
-  P.data_max = regions_max + 8 * ds_ptr.size();  // 16-byte alignment padding per region
+  P.data_max = regions_max;
   return regions_max + 16 * 1024 <= kSmemMax;
 }
 
@@ -1483,6 +1615,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         LT_CK_LAUNCH();
         D.a[d].slot = LP.slots[d].get();
         D.a[d].ds = ds_of[a + d];
+        D.a[d].sstride = D.a[d].vpe | 1;
       }
     }
     if (!LP.inc_desc.empty()) {
@@ -1531,6 +1664,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         IP.slots = LP.inc[p].slots.get();
       }
       D.n_inc = (int)LP.inc_desc.size();
+      D.n_plans = (int)LP.plan_map.size();
     }
     a += D.n_desc;
   }
@@ -1551,9 +1685,14 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     for (size_t k = 0; k < ds_ptr.size(); ++k) {
       H.ds[k].data = ds_ptr[k];
       H.ds[k].vpe = ds_vpe[k];
+      H.ds[k].stride = ds_vpe[k] | 1;
       H.ds[k].sp = sp_index.at(ds_space[k]);
       H.ds[k].load = 1;
+      H.ds[k].ro = 1;
     }
+    for (int j = 0, q = 0; j < nl; ++j)
+      for (size_t d = 0; d < cv.loops[j].desc.size(); ++d, ++q)
+        if (cv.loops[j].desc[d].mode != LT_READ) H.ds[ds_of[q]].ro = 0;
     a = 0;
     for (int j = 0; j < nl; ++j) {
       const LoopDesc &L = cv.loops[j];
@@ -1565,7 +1704,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
           const Footprint &fp = P.fp.at(ds_space[k]);
           P.wflags[k].alloc(std::max<int64_t>(fp.off_host.back(), 1), ctx.stream);
           LT_CK(cudaMemsetAsync(P.wflags[k].get(), 0, P.wflags[k].n, ctx.stream));
-          H.ds[k].wflag = P.wflags[k].get();
+          H.ds[k].written = 1;
         }
         const int ar = L.desc[d].map < 0 ? 1 : cv.maps[L.desc[d].map].arity;
         if (Lj.n)
@@ -1835,6 +1974,17 @@ extern "C" int lt_kernel_lookup(const char *name, int32_t *kernel_id, int32_t *n
 }
 
 extern "C" int lt_kernel_count(void) { return kNumKernels; }
+
+#ifdef LT_PHASE_TIMING
+extern "C" int lt_phase_cycles(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 40);
+  if (reset) {
+    static unsigned long long zero[40] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif
 
 extern "C" const char *lt_kernel_name(int32_t id) {
   return (id >= 0 && id < kNumKernels) ? kSpecs[id].name : nullptr;

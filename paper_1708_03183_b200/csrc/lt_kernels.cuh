@@ -47,7 +47,7 @@ struct DArg {
   int32_t inc_off;      // tiled: offset (doubles) of this descriptor's slots in smem
   const int32_t *slot;  // staged: footprint slot per list position (direct) or (position, k)
   int32_t ds;           // staged: index of the staged dataset this descriptor binds
-  int32_t pad;
+  int32_t sstride;      // staged: shared-memory row stride (odd: conflict-free 64-bit rows)
 };
 
 #define LT_MAX_STAGED 16  // distinct datasets staged in shared memory
@@ -60,11 +60,12 @@ struct DArg {
 
 struct StageDS {
   double *data;
-  const uint8_t *wflag;    // per footprint entry: written by the tile (nullptr: read-only)
   int32_t vpe;
+  int32_t stride;          // shared-memory row stride (vpe | 1)
   int32_t sp;              // footprint space index
   int32_t load;            // 0: every footprint row is written before it is read
-  int32_t pad;
+  int32_t written;         // the tile writes some rows of it (store-back flags present)
+  int32_t ro;              // never written by the chain: gathered before dependency waits
 };
 
 struct IncPlan {
@@ -83,6 +84,8 @@ struct DLoop {
   int32_t n_inc;
   int32_t use_local;
   int32_t exec_size;
+  int32_t n_plans;          // staged: distinct ordered-gather plans (maps) of the loop
+  int32_t pad2;
   const double *params;
   const int32_t *offsets;   // tiled: per-tile list offsets
   const int32_t *elements;  // tiled: concatenated lists

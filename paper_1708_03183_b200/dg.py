@@ -28,7 +28,7 @@ adjacency map (SURVEY section 7 "Seed adjacency for DG").
 
 Data layout (element-major, like the reference Dataset): u = [vx(nd), vy(nd)],
 s = [sxx(nd), syy(nd), sxy(nd)], cgeo = [rx, ry, sx, sy, detJ],
-mat = [rho, lambda, mu], fgeo = [nx, ny, |f|/2, face_a, face_b] (face_b = -1 on
+mat = [rho, lambda, mu, Zp, Zs] (impedances rho*c_p, rho*c_s precomputed), fgeo = [nx, ny, |f|/2, face_a, face_b] (face_b = -1 on
 exterior facets).  The operator tables (``dg_tables``) are generated once in
 float64 and are the same arrays the CUDA kernels and the CPU oracle use.
 """
@@ -240,6 +240,9 @@ def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
     if dt is None:
         cp = np.sqrt((mat[:, 1] + 2 * mat[:, 2]) / mat[:, 0]).max()
         dt = 0.1 * 1.0 / (cp * (2 * p + 1))
+    zp = np.sqrt(mat[:, 0] * (mat[:, 1] + 2 * mat[:, 2]))
+    zs = np.sqrt(mat[:, 0] * mat[:, 2])
+    mat = np.column_stack([mat, zp, zs])
     # initial condition: Gaussian pulse at the domain centre on all components
     X = mesh.vertex_coords
     centre = ((X[:, 0].min() + X[:, 0].max()) / 2, (X[:, 1].min() + X[:, 1].max()) / 2)
@@ -253,7 +256,7 @@ def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
         "ru": np.zeros(C * 2 * nd), "rs": np.zeros(C * 3 * nd),
         "figeo": fig.ravel(), "fegeo": feg.ravel(),
     }
-    vpe = {"cgeo": 5, "mat": 3, "u": 2 * nd, "s": 3 * nd, "ru": 2 * nd, "rs": 3 * nd,
+    vpe = {"cgeo": 5, "mat": 5, "u": 2 * nd, "s": 3 * nd, "ru": 2 * nd, "rs": 3 * nd,
            "figeo": 5, "fegeo": 5}
     space_of = {"cgeo": CELLS, "mat": CELLS, "u": CELLS, "s": CELLS, "ru": CELLS, "rs": CELLS,
                 "figeo": IFACETS, "fegeo": EFACETS}
