@@ -41,7 +41,7 @@ from functools import lru_cache
 import numpy as np
 
 from .chain import AccessMode, Descriptor, IterationSpace, Loop, MeshMap, build_chain
-from .mesh import (CELLS, EFACETS, IFACETS, VERTS, Mesh, cell_edge_map, facet_topology,
+from .mesh import (CELLS, EDGES, EFACETS, IFACETS, VERTS, Mesh, cell_edge_map, facet_topology,
                    generate_rect_mesh, renumber)
 
 R, W, I, RW = AccessMode.READ, AccessMode.WRITE, AccessMode.INC, AccessMode.RW
@@ -171,6 +171,9 @@ class ElasticSetup:
     space_of: dict      # dataset -> space name
     tables: DGTables
     chain: object = None
+    facets: object = None       # global FacetTopology (for rank-local restriction)
+    local_mesh: object = None   # set on rank-local setups
+    global_ids: dict | None = None
 
     @property
     def n_cells(self) -> int:
@@ -262,7 +265,49 @@ def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
                 "figeo": IFACETS, "fegeo": EFACETS}
     loops, bindings = chain_loops(p, steps_per_chain, spaces, maps)
     return ElasticSetup(p, mesh, steps_per_chain, float(dt), spaces, maps, loops, bindings,
-                        data, vpe, space_of, tab)
+                        data, vpe, space_of, tab, facets=ft)
+
+
+def local_elastic_setup(setup: ElasticSetup, lm) -> ElasticSetup:
+    """Restrict a global elastic instance to one rank's extended-halo mesh.
+
+    Cells keep the partition's region order (core | owned+exec | non-exec);
+    local edges split into interior/exterior facets by their *global* flank
+    count, flank maps through local ids, a missing flank pointing at the
+    present cell (only possible in the non-exec strip).
+    Dataset rows are the global rows of the local elements, so halo rows of
+    constant data (geometry, material) are exact without any exchange.
+    """
+    ft = setup.facets
+    iid, if2c, eid, ef2c, isz, esz = lm.facets()
+    egid = lm.global_ids[EDGES]
+    # global facet index of every global edge
+    inv_i = np.full(setup.mesh.num_edges, -1, dtype=np.int64)
+    inv_i[ft.iedge] = np.arange(ft.n_interior)
+    inv_e = np.full(setup.mesh.num_edges, -1, dtype=np.int64)
+    inv_e[ft.eedge] = np.arange(ft.n_exterior)
+    gi, ge = inv_i[egid[iid]], inv_e[egid[eid]]
+    assert np.all(gi >= 0) and np.all(ge >= 0)
+    cs, vs = lm.sizes[CELLS], lm.sizes[VERTS]
+    spaces = {CELLS: IterationSpace(CELLS, cs.core, cs.owned + cs.exec, cs.nonexec),
+              IFACETS: IterationSpace(IFACETS, *isz),
+              EFACETS: IterationSpace(EFACETS, *esz),
+              VERTS: IterationSpace(VERTS, vs.core, vs.owned + vs.exec, vs.nonexec)}
+    maps = {
+        "c2v": MeshMap("c2v", spaces[CELLS], spaces[VERTS], 3, lm.cells_to_vertices),
+        "if2c": MeshMap("if2c", spaces[IFACETS], spaces[CELLS], 2, if2c),
+        "ef2c": MeshMap("ef2c", spaces[EFACETS], spaces[CELLS], 1, ef2c),
+    }
+    cg = lm.global_ids[CELLS]
+    rows = {CELLS: cg, IFACETS: gi, EFACETS: ge}
+    data = {n: v.reshape(-1, setup.vpe[n])[rows[setup.space_of[n]]].ravel().copy()
+            for n, v in setup.data.items()}
+    loops, bindings = chain_loops(setup.p, setup.steps_per_chain, spaces, maps)
+    local = ElasticSetup(setup.p, setup.mesh, setup.steps_per_chain, setup.dt, spaces, maps,
+                         loops, bindings, data, dict(setup.vpe), dict(setup.space_of),
+                         setup.tables, facets=None, local_mesh=lm,
+                         global_ids={CELLS: cg, IFACETS: gi, EFACETS: ge})
+    return local
 
 
 def chain_loops(p, steps, spaces, maps, loop_cls=Loop, desc_cls=Descriptor, binding_cls=None,
@@ -378,3 +423,61 @@ def compulsory_bytes(chain, bindings, vpe: dict, space_total: dict) -> int:
         if name in written:
             total += size
     return total + sum(maps.values())
+
+
+def constant_datasets(chain, bindings) -> set[str]:
+    """Datasets no loop of the chain writes (their halo rows never go stale)."""
+    written = {n for lp, b in zip(chain.loops, bindings)
+               for d, n in zip(lp.descriptors, b.args) if d.mode is not AccessMode.READ}
+    return {n for b in bindings for n in b.args} - written
+
+
+def run_elastic_distributed(setup: ElasticSetup, nranks: int, depth: int, ts: int,
+                            n_chains: int = 1, mode=None, poison_halo: bool = False,
+                            use_local_maps: bool = True):
+    """The elastic chain on ``nranks`` virtual ranks sharing one GPU.
+
+    Partition (strips + ``depth`` halo strips), rank-local problems, mixed-mode
+    (SHARED) inspection per rank, one halo exchange per chain execution
+    (reference ``distsim.run_distributed`` semantics; constant datasets are not
+    exchanged).  Returns the gathered owned rows of ``u`` and ``s``.
+    """
+    from .distributed import (HaloEndpoint, _PreStaged, check_exchange_symmetry,
+                              exchanged_from_chain)
+    from .executor import execute_schedule
+    from .inspector import ExecMode
+    from .partition import partition_for_ranks
+    mode = mode or ExecMode.SHARED
+    ranks = []
+    for lm in partition_for_ranks(setup.mesh, nranks, depth):
+        loc = local_elastic_setup(setup, lm)
+        pb = elastic_problem(loc, depth=len(loc.loops))
+        owned = lm.sizes[CELLS].owned_total
+        if poison_halo:
+            for n in ("u", "s", "ru", "rs"):
+                pb.datasets[n].values[owned * loc.vpe[n]:] = 1e30
+        sched = pb.inspect(ts, mode)
+        const = constant_datasets(pb.chain, pb.bindings)
+        exchanged = tuple(n for n in exchanged_from_chain(pb.chain, pb.bindings) if n not in const)
+        ranks.append((lm, pb, sched, HaloEndpoint(lm, pb.datasets, exchanged)))
+    eps = [r[3] for r in ranks]
+    for e in eps:
+        e.link(eps)
+    check_exchange_symmetry(eps)
+    ranks[0][1].install_params()
+    for _ in range(n_chains):
+        for e in eps:
+            e.begin()
+        for lm, pb, sched, ep in ranks:
+            execute_schedule(sched, pb.chain, pb.bindings, pb.datasets, pb.registry,
+                             exchange=_PreStaged(ep), use_local_maps=use_local_maps)
+    out = {}
+    for n in ("u", "s"):
+        k = setup.vpe[n]
+        vals = np.full(setup.mesh.num_cells * k, np.nan)
+        for lm, pb, _, _ in ranks:
+            owned = lm.sizes[CELLS].owned_total
+            vals.reshape(-1, k)[lm.global_ids[CELLS][:owned]] = \
+                pb.datasets[n].numpy().reshape(-1, k)[:owned]
+        out[n] = vals
+    return out, ranks

@@ -35,3 +35,19 @@ def test_gpu_eight_loop_distributed_equals_serial(nranks, depth):
                           mode=lt.ExecMode.SHARED)
     for n, v in res.datasets.items():
         np.testing.assert_array_equal(v, ds[n].numpy(), err_msg=n)
+
+
+@pytest.mark.parametrize("p,steps,nranks", [(1, 1, 2), (1, 2, 3), (2, 1, 4)])
+def test_gpu_elastic_distributed_equals_serial(p, steps, nranks):
+    from paper_1708_03183_b200.dg import elastic_problem, elastic_setup, run_elastic_distributed
+    st = elastic_setup(24, 20, p, steps, material=("uniform", 3), sigma=4.0)
+    serial = elastic_problem(elastic_setup(24, 20, p, steps, material=("uniform", 3), sigma=4.0))
+    serial.run_untiled(n_chains=2)
+    got, ranks = run_elastic_distributed(st, nranks, depth=5 * steps, ts=16, n_chains=2,
+                                         poison_halo=True)
+    for n in ("u", "s"):
+        ref = serial.datasets[n].numpy()
+        assert np.all(np.isfinite(got[n])), n
+        err = np.max(np.abs(got[n] - ref)) / np.max(np.abs(ref))
+        assert err <= 1e-12, (n, err)
+    assert all(r[3].exchange_count == 2 for r in ranks)
