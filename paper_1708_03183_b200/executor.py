@@ -343,6 +343,18 @@ class TiledRunner:
         return self._lib.execute_repeat(self.handle, self.bound.desc, self.bound.args,
                                         self.repeats, self.use_local_maps)
 
+    def with_exchange(self, exchange):
+        """One chain execution around a halo exchange (Alg. 2 order):
+        ``begin()``, core colour classes, ``end()``, boundary colour classes."""
+        lib = self._lib
+        exchange.begin()
+        a = lib.execute(self.handle, self.bound.desc, self.bound.args, lib.PHASE_CORE,
+                        self.use_local_maps)
+        exchange.end()
+        b = lib.execute(self.handle, self.bound.desc, self.bound.args, lib.PHASE_BOUNDARY,
+                        self.use_local_maps)
+        return a.launches + b.launches
+
     def graph(self, repeats: int = 1):
         """CUDA graph replaying ``repeats`` chain executions back to back."""
         import torch
