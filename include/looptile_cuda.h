@@ -192,6 +192,41 @@ int lt_schedule_tile_of(const lt_schedule *s, int32_t loop, const int32_t **devi
 int lt_schedule_local_map(const lt_schedule *s, int32_t loop, int32_t map, int32_t *out);
 int lt_schedule_destroy(lt_schedule *s);
 
+/* ---- step-level inspector (the public steps of inspector.py) -----------------
+ * Tile pairs are encoded (a << 32) | b with a < b; *n_pairs receives the
+ * total, at most `capacity` are written to `pairs` (host). */
+/* partition_seed (inspector.py:185-205): sigma device int32[space total] */
+int lt_partition_seed(lt_ctx *ctx, const lt_space *space, int64_t tile_size, int32_t *sigma,
+                      int32_t *n_core_tiles, int32_t *n_boundary_tiles);
+/* assign (inspector.py:385-391): device offsets int32[n_tiles+1], elements int32[n] */
+int lt_assign(lt_ctx *ctx, const int32_t *sigma, int64_t n, int32_t n_tiles, int32_t *offsets,
+              int32_t *elements);
+/* _seed_adjacency (inspector.py:208-225): tiles sharing a target of the seed map */
+int lt_seed_adjacency(lt_ctx *ctx, const int32_t *map_values, int64_t n_source, int32_t arity,
+                      int64_t n_target, const int32_t *sigma, int32_t n_tiles, int64_t *pairs,
+                      int64_t capacity, int64_t *n_pairs);
+/* color_tiles (inspector.py:228-263), host only: regions host int32[n_tiles],
+ * pairs = adjacency (seed adjacency + fake connections), colors host out */
+int lt_color_tiles(int32_t n_tiles, const int32_t *regions, int32_t mode, const int64_t *pairs,
+                   int64_t n_pairs, int32_t *colors);
+/* project (inspector.py:266-316) of loop `loop`: phi[s] = device int32[space s total]
+ * per chain space, present[s] (host) says whether phi[s] holds a projection;
+ * both are updated; conflict pairs returned */
+int lt_project(lt_ctx *ctx, const lt_chain *chain, int32_t loop, const int32_t *sigma,
+               const int32_t *colors, int32_t n_tiles, int32_t *const *phi, int32_t *present,
+               int64_t *pairs, int64_t capacity, int64_t *n_pairs);
+/* tile_loop (inspector.py:319-382): sigma_out device int32[space total];
+ * tne >= 0 forces non-exec elements to tile tne (inspect_chain :480);
+ * detect != 0 runs the second (conflict) sweep */
+int lt_tile_loop(lt_ctx *ctx, const lt_chain *chain, int32_t loop, int32_t *const *phi,
+                 const int32_t *present, const int32_t *colors, int32_t n_tiles, int32_t tne,
+                 int32_t *sigma_out, int32_t detect, int64_t *pairs, int64_t capacity,
+                 int64_t *n_pairs);
+
+/* compute_local_maps (inspector.py:397-418): out[p*arity+k] = map[elements[p]*arity+k] */
+int lt_gather_rows(lt_ctx *ctx, const int32_t *map_values, int32_t arity, const int32_t *elements,
+                   int64_t n, int32_t *out);
+
 /* ---- executor (executor.py:163-245) ---------------------------------------- */
 /* args: flat lt_arg array, loop-major, one per descriptor.
  * execute_schedule: run the selected phases (LT_PHASE_CORE|LT_PHASE_BOUNDARY);

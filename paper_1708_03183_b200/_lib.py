@@ -116,6 +116,16 @@ SIGNATURES = {
     "lt_halo_pack": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int64, _P]),
     "lt_halo_unpack": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int64, _P]),
     "lt_rcm_order": (C.c_int, [C.c_int64, _P, _P, _P]),
+    "lt_gather_rows": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int64, _P]),
+    "lt_partition_seed": (C.c_int, [_P, C.POINTER(LtSpace), C.c_int64, _P, _I32P, _I32P]),
+    "lt_assign": (C.c_int, [_P, _P, C.c_int64, C.c_int32, _P, _P]),
+    "lt_seed_adjacency": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int64, _P, C.c_int32, _P,
+                                    C.c_int64, _I64P]),
+    "lt_color_tiles": (C.c_int, [C.c_int32, _P, C.c_int32, _P, C.c_int64, _P]),
+    "lt_project": (C.c_int, [_P, C.POINTER(LtChain), C.c_int32, _P, _P, C.c_int32,
+                             C.POINTER(_P), _P, _P, C.c_int64, _I64P]),
+    "lt_tile_loop": (C.c_int, [_P, C.POINTER(LtChain), C.c_int32, C.POINTER(_P), _P, _P,
+                               C.c_int32, C.c_int32, _P, C.c_int32, _P, C.c_int64, _I64P]),
 }
 
 _lib = None
@@ -345,6 +355,138 @@ def import_schedule(chain, mode_code: int, colors, regions, rounds: int,
                                     col.ctypes.data, reg.ctypes.data, rounds, offs, elems,
                                     C.byref(h)))
     return ScheduleHandle(h, ctx, cd)
+
+
+# ---- step-level inspector ------------------------------------------------------------
+
+def _dev_i32(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(
+        torch.device("cuda", torch.cuda.current_device()))
+
+
+def _pairs_call(fn, *args):
+    cap = 1 << 16
+    while True:
+        buf = np.empty(cap, dtype=np.int64)
+        n = C.c_int64()
+        check(fn(*args, buf.ctypes.data, cap, C.byref(n)))
+        if n.value <= cap:
+            v = buf[:n.value]
+            return [(int(x >> 32), int(x & 0xffffffff)) for x in v]
+        cap = n.value
+
+
+def partition_seed(space, ts: int) -> tuple[np.ndarray, int, int]:
+    import torch
+    ctx = context()
+    sig = torch.empty(max(space.total, 1), dtype=torch.int32, device="cuda")
+    m, k = C.c_int32(), C.c_int32()
+    sp = LtSpace(space.core_size, space.boundary_size, space.nonexec_size)
+    check(load().lt_partition_seed(ctx.bind_stream(), C.byref(sp), int(ts), sig.data_ptr(),
+                                   C.byref(m), C.byref(k)))
+    return sig[:space.total].cpu().numpy().astype(np.int64), m.value, k.value
+
+
+def assign(sigma: np.ndarray, n_tiles: int) -> tuple[np.ndarray, np.ndarray]:
+    import torch
+    ctx = context()
+    s = _dev_i32(sigma)
+    off = torch.empty(n_tiles + 1, dtype=torch.int32, device="cuda")
+    el = torch.empty(max(len(sigma), 1), dtype=torch.int32, device="cuda")
+    check(load().lt_assign(ctx.bind_stream(), s.data_ptr(), len(sigma), n_tiles, off.data_ptr(),
+                           el.data_ptr()))
+    return off.cpu().numpy().astype(np.int64), el[:len(sigma)].cpu().numpy().astype(np.int64)
+
+
+def seed_adjacency(seed_map, sigma0: np.ndarray, n_tiles: int) -> list[tuple[int, int]]:
+    ctx = context()
+    vals = seed_map.device_values()
+    s = _dev_i32(sigma0)
+    return _pairs_call(load().lt_seed_adjacency, ctx.bind_stream(), vals.data_ptr(),
+                       seed_map.source.total, seed_map.arity, seed_map.target.total, s.data_ptr(),
+                       n_tiles)
+
+
+def color_tiles(regions, mode_code: int, pairs) -> np.ndarray:
+    reg = np.ascontiguousarray(regions, dtype=np.int32)
+    pr = np.array([(a << 32) | b for a, b in pairs] or [0], dtype=np.int64)
+    out = np.empty(len(reg), dtype=np.int32)
+    check(load().lt_color_tiles(len(reg), reg.ctypes.data, mode_code, pr.ctypes.data,
+                                len(pairs), out.ctypes.data))
+    return out
+
+
+class LoopChainDesc:
+    """ctypes image of a one-loop chain (the loop's spaces and maps)."""
+
+    def __init__(self, loop):
+        import types
+        spaces, maps = [loop.space], []
+        for d in loop.descriptors:
+            if d.map is not None:
+                if all(m is not d.map for m in maps):
+                    maps.append(d.map)
+                for sp in (d.map.source, d.map.target):
+                    if sp not in spaces:
+                        spaces.append(sp)
+        from .chain import Loop
+        fake = types.SimpleNamespace(spaces=tuple(spaces), maps=tuple(maps), depth=1,
+                                     loops=(Loop(0, loop.space, loop.descriptors, loop.kernel),))
+        self.desc = ChainDesc(fake)
+        self.spaces = spaces
+
+
+def project(loop, sigma: np.ndarray, colors: np.ndarray, phi: dict) -> list[tuple[int, int]]:
+    """phi: space name -> int64 numpy assignment (updated in place)."""
+    import torch
+    ctx = context()
+    lc = LoopChainDesc(loop)
+    bufs, present = [], np.zeros(len(lc.spaces), dtype=np.int32)
+    for i, sp in enumerate(lc.spaces):
+        if sp.name in phi:
+            bufs.append(_dev_i32(phi[sp.name]))
+            present[i] = 1
+        else:
+            bufs.append(torch.full((max(sp.total, 1),), -1, dtype=torch.int32, device="cuda"))
+    ptrs = (C.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+    sig, col = _dev_i32(sigma), _dev_i32(colors)
+    pairs = _pairs_call(load().lt_project, ctx.bind_stream(), lc.desc.ref, 0, sig.data_ptr(),
+                        col.data_ptr(), len(colors), ptrs, present.ctypes.data)
+    for i, sp in enumerate(lc.spaces):
+        if present[i]:
+            phi[sp.name] = bufs[i][:sp.total].cpu().numpy().astype(np.int64)
+    return pairs
+
+
+def tile_loop(loop, colors: np.ndarray, phi: dict, detect: bool, tne: int = -1):
+    import torch
+    ctx = context()
+    lc = LoopChainDesc(loop)
+    bufs, present = [], np.zeros(len(lc.spaces), dtype=np.int32)
+    for i, sp in enumerate(lc.spaces):
+        if sp.name in phi:
+            bufs.append(_dev_i32(phi[sp.name]))
+            present[i] = 1
+        else:
+            bufs.append(torch.full((max(sp.total, 1),), -1, dtype=torch.int32, device="cuda"))
+    ptrs = (C.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+    col = _dev_i32(colors)
+    out = torch.empty(max(loop.space.total, 1), dtype=torch.int32, device="cuda")
+    pairs = _pairs_call(load().lt_tile_loop, ctx.bind_stream(), lc.desc.ref, 0, ptrs,
+                        present.ctypes.data, col.data_ptr(), len(colors), tne, out.data_ptr(),
+                        int(detect))
+    return out[:loop.space.total].cpu().numpy().astype(np.int64), pairs
+
+
+def gather_rows(mesh_map, elements: np.ndarray) -> np.ndarray:
+    import torch
+    ctx = context()
+    el = _dev_i32(elements)
+    out = torch.empty(max(len(elements) * mesh_map.arity, 1), dtype=torch.int32, device="cuda")
+    check(load().lt_gather_rows(ctx.bind_stream(), mesh_map.device_values().data_ptr(),
+                                mesh_map.arity, el.data_ptr(), len(elements), out.data_ptr()))
+    return out[:len(elements) * mesh_map.arity].cpu().numpy().astype(np.int64)
 
 
 # ---- executor ---------------------------------------------------------------------------

@@ -235,9 +235,10 @@ __global__ void k_seed_adjacency(const int32_t *inv_off, const int32_t *inv_flat
   int b = inv_off[g], e = inv_off[g + 1];
   for (int i = b; i < e; ++i) {
     int ti = sigma0[inv_flat[i] / arity];
+    if (ti < 0) continue;  // element in no seed list
     for (int j = i + 1; j < e; ++j) {
       int tj = sigma0[inv_flat[j] / arity];
-      if (ti != tj) pair_insert(ps, ti, tj);
+      if (tj >= 0 && ti != tj) pair_insert(ps, ti, tj);
     }
   }
 }
@@ -316,7 +317,7 @@ __global__ void k_tile_loop(Candidates cand, const int32_t *colors, int64_t tota
   if (e < exec_size) {
     if (held < 0) {
       atomicMin(first_missing, (int)e);
-    } else {
+    } else if (ps.keys) {  // second sweep only when conflicts are collected
       for (int d = 0; d < cand.n; ++d) {
         const int32_t *pa = cand.proj[d];
         const int32_t *mp = cand.map[d];
@@ -329,7 +330,7 @@ __global__ void k_tile_loop(Candidates cand, const int32_t *colors, int64_t tota
     }
     sigma_out[e] = held;
   } else {
-    sigma_out[e] = tne;
+    sigma_out[e] = tne >= 0 ? tne : held;
   }
 }
 
@@ -763,5 +764,211 @@ extern "C" int lt_schedule_local_map(const lt_schedule *s, int32_t loop, int32_t
 extern "C" int lt_schedule_destroy(lt_schedule *s) {
   LT_API_BEGIN
   delete s;
+  LT_API_END
+}
+
+// ---- step-level inspector API (reference inspector.py public functions) -------
+
+namespace lt {
+
+static void copy_pairs(PairTable &pt, int64_t *pairs, int64_t cap, int64_t *n_pairs) {
+  std::vector<unsigned long long> v = pt.fetch();
+  *n_pairs = (int64_t)v.size();
+  if (pairs)
+    for (int64_t i = 0; i < (int64_t)v.size() && i < cap; ++i) pairs[i] = (int64_t)v[i];
+}
+
+static unsigned int pair_capacity(int n_tiles) {
+  return pow2_at_least(int64_t(std::max(n_tiles, 1)) * 64);
+}
+
+}  // namespace lt
+
+extern "C" int lt_partition_seed(lt_ctx *ctx, const lt_space *sp, int64_t ts, int32_t *sigma,
+                                 int32_t *n_core_tiles, int32_t *n_boundary_tiles) {
+  LT_API_BEGIN
+  if (!ctx || !sp) fail(LT_E_VALUE, "null argument");
+  if (ts < 1) fail(LT_E_VALUE, "tile size must be >= 1, got " + std::to_string(ts));
+  const int64_t m = (sp->core + ts - 1) / ts, k = (sp->boundary + ts - 1) / ts;
+  const int64_t total = sp->core + sp->boundary + sp->nonexec;
+  if (total)
+    k_partition_seed<<<grid_for(total, 256), 256, 0, ctx->stream>>>(sigma, sp->core, sp->boundary,
+                                                                     total, ts, (int)m, (int)k);
+  LT_CK_LAUNCH();
+  LT_CK(cudaStreamSynchronize(ctx->stream));
+  *n_core_tiles = (int32_t)m;
+  *n_boundary_tiles = (int32_t)k;
+  LT_API_END
+}
+
+extern "C" int lt_assign(lt_ctx *ctx, const int32_t *sigma, int64_t n, int32_t n_tiles,
+                         int32_t *offsets, int32_t *elements) {
+  LT_API_BEGIN
+  if (!ctx) fail(LT_E_VALUE, "null context");
+  LoopLists L;
+  assign_lists(*ctx, sigma, n, n_tiles, L);
+  LT_CK(cudaMemcpyAsync(offsets, L.offsets.get(), 4 * (n_tiles + 1), cudaMemcpyDeviceToDevice,
+                        ctx->stream));
+  if (n)
+    LT_CK(cudaMemcpyAsync(elements, L.elements.get(), 4 * n, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  LT_CK(cudaStreamSynchronize(ctx->stream));
+  LT_API_END
+}
+
+extern "C" int lt_seed_adjacency(lt_ctx *ctx, const int32_t *values, int64_t n_source,
+                                 int32_t arity, int64_t n_target, const int32_t *sigma,
+                                 int32_t n_tiles, int64_t *pairs, int64_t capacity,
+                                 int64_t *n_pairs) {
+  LT_API_BEGIN
+  if (!ctx) fail(LT_E_VALUE, "null context");
+  DevBuf<int32_t> off(n_target + 1, ctx->stream), flat(n_source * arity, ctx->stream);
+  invert_flat(*ctx, values, n_source, arity, n_target, off.get(), flat.get());
+  PairTable pt(*ctx, pair_capacity(n_tiles));
+  for (;;) {
+    if (n_target)
+      k_seed_adjacency<<<grid_for(n_target, 256), 256, 0, ctx->stream>>>(
+          off.get(), flat.get(), arity, sigma, n_target, pt.view());
+    LT_CK_LAUNCH();
+    if (pt.status().second) { pt.resize(pt.cap * 2); continue; }
+    break;
+  }
+  copy_pairs(pt, pairs, capacity, n_pairs);
+  LT_API_END
+}
+
+extern "C" int lt_color_tiles(int32_t n_tiles, const int32_t *regions, int32_t mode,
+                              const int64_t *pairs, int64_t n_pairs, int32_t *colors) {
+  LT_API_BEGIN
+  if (n_tiles < 1) fail(LT_E_VALUE, "no tiles");
+  std::vector<int32_t> region(regions, regions + n_tiles), color(n_tiles, -1);
+  std::vector<std::vector<int>> adj(n_tiles);
+  for (int64_t i = 0; i < n_pairs; ++i) {
+    const int a = (int)(pairs[i] >> 32), b = (int)(pairs[i] & 0xffffffff);
+    if (a < 0 || b < 0 || a >= n_tiles || b >= n_tiles) fail(LT_E_VALUE, "pair outside tiles");
+    adj[a].push_back(b);
+    adj[b].push_back(a);
+  }
+  color_tiles_host(mode, region, adj, color);
+  std::copy(color.begin(), color.end(), colors);
+  LT_API_END
+}
+
+extern "C" int lt_project(lt_ctx *ctx, const lt_chain *chain, int32_t loop, const int32_t *sigma,
+                          const int32_t *colors, int32_t n_tiles, int32_t *const *phi,
+                          int32_t *present, int64_t *pairs, int64_t capacity, int64_t *n_pairs) {
+  LT_API_BEGIN
+  if (!ctx || !chain || !phi || !present) fail(LT_E_VALUE, "null argument");
+  ChainView cv(chain);
+  if (loop < 0 || loop >= (int)cv.loops.size()) fail(LT_E_VALUE, "bad loop index");
+  const LoopDesc &L = cv.loops[loop];
+  PairTable pt(*ctx, pair_capacity(n_tiles));
+  std::vector<int32_t> pres(present, present + cv.spaces.size());
+  for (;;) {
+    // replay from the caller's projections each attempt (inputs stay untouched)
+    std::map<int, DevBuf<int32_t>> cur;
+    std::vector<char> have(cv.spaces.size());
+    for (size_t sp = 0; sp < cv.spaces.size(); ++sp) have[sp] = pres[sp] != 0;
+    auto view = [&](int sp) -> const int32_t * {
+      auto it = cur.find(sp);
+      return it != cur.end() ? it->second.get() : phi[sp];
+    };
+    for (const lt_desc &d : L.desc) {
+      if (d.map < 0) {
+        const int sp = L.space;
+        const int64_t n = cv.total(sp);
+        if (have[sp] && n)
+          k_project_direct<<<grid_for(n, 256), 256, 0, ctx->stream>>>(view(sp), sigma, colors, n,
+                                                                      pt.view());
+        LT_CK_LAUNCH();
+        DevBuf<int32_t> nb(n, ctx->stream);
+        if (n)
+          LT_CK(cudaMemcpyAsync(nb.get(), sigma, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        cur[sp] = std::move(nb);
+        have[sp] = 1;
+      } else {
+        const lt_map &mp = cv.maps[d.map];
+        const int sp = mp.target;
+        const int64_t ns = cv.total(mp.source), nt = cv.total(sp);
+        DevBuf<int32_t> off(nt + 1, ctx->stream), flat(ns * mp.arity, ctx->stream), nb(nt, ctx->stream);
+        invert_flat(*ctx, mp.values, ns, mp.arity, nt, off.get(), flat.get());
+        if (nt)
+          k_project_mapped<<<grid_for(nt, 256), 256, 0, ctx->stream>>>(
+              off.get(), flat.get(), mp.arity, sigma, colors, have[sp] ? view(sp) : nullptr,
+              nb.get(), nt, pt.view());
+        LT_CK_LAUNCH();
+        cur[sp] = std::move(nb);
+        have[sp] = 1;
+      }
+    }
+    if (pt.status().second) { pt.resize(pt.cap * 2); continue; }
+    for (auto &kv : cur) {
+      const int64_t n = cv.total(kv.first);
+      if (n)
+        LT_CK(cudaMemcpyAsync(phi[kv.first], kv.second.get(), 4 * n, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+      present[kv.first] = 1;
+    }
+    break;
+  }
+  copy_pairs(pt, pairs, capacity, n_pairs);
+  LT_API_END
+}
+
+extern "C" int lt_tile_loop(lt_ctx *ctx, const lt_chain *chain, int32_t loop,
+                            int32_t *const *phi, const int32_t *present, const int32_t *colors,
+                            int32_t n_tiles, int32_t tne, int32_t *sigma_out, int32_t detect,
+                            int64_t *pairs, int64_t capacity, int64_t *n_pairs) {
+  LT_API_BEGIN
+  if (!ctx || !chain || !phi || !present) fail(LT_E_VALUE, "null argument");
+  ChainView cv(chain);
+  if (loop < 0 || loop >= (int)cv.loops.size()) fail(LT_E_VALUE, "bad loop index");
+  const LoopDesc &L = cv.loops[loop];
+  Candidates cand{};
+  for (const lt_desc &d : L.desc) {
+    const int sp = d.map < 0 ? L.space : cv.maps[d.map].target;
+    if (!present[sp]) continue;
+    if (cand.n >= LT_MAX_DESC) fail(LT_E_INSPECTION, "too many descriptors");
+    cand.proj[cand.n] = phi[sp];
+    cand.map[cand.n] = d.map < 0 ? nullptr : cv.maps[d.map].values;
+    cand.arity[cand.n] = d.map < 0 ? 1 : cv.maps[d.map].arity;
+    cand.n++;
+  }
+  if (cand.n == 0)
+    fail(LT_E_INSPECTION, "loop " + std::to_string(loop) + " over space " +
+                              std::to_string(L.space) + ": no projection covers any accessed space");
+  const int64_t n = cv.total(L.space);
+  PairTable pt(*ctx, pair_capacity(n_tiles));
+  DevBuf<int> missing(1, ctx->stream);
+  for (;;) {
+    const int big = 0x7fffffff;
+    LT_CK(cudaMemcpyAsync(missing.get(), &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    PairSet ps = pt.view();
+    if (!detect) ps.keys = nullptr;
+    if (n)
+      k_tile_loop<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cand, colors, n, cv.exec_size(L.space),
+                                                             tne, sigma_out, missing.get(), ps);
+    LT_CK_LAUNCH();
+    int miss = big;
+    LT_CK(cudaMemcpyAsync(&miss, missing.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LT_CK(cudaStreamSynchronize(ctx->stream));
+    if (miss != big)
+      fail(LT_E_INSPECTION, "loop " + std::to_string(loop) + ": element " + std::to_string(miss) +
+                                " of space " + std::to_string(L.space) +
+                                " is not reachable through any projection");
+    if (detect && pt.status().second) { pt.resize(pt.cap * 2); continue; }
+    break;
+  }
+  if (detect) copy_pairs(pt, pairs, capacity, n_pairs);
+  else *n_pairs = 0;
+  LT_API_END
+}
+
+extern "C" int lt_gather_rows(lt_ctx *ctx, const int32_t *map_values, int32_t arity,
+                              const int32_t *elements, int64_t n, int32_t *out) {
+  LT_API_BEGIN
+  if (!ctx) fail(LT_E_VALUE, "null context");
+  gather_rows(*ctx, map_values, arity, elements, n, out);
+  LT_CK(cudaStreamSynchronize(ctx->stream));
   LT_API_END
 }

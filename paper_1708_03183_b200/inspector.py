@@ -276,6 +276,118 @@ class Schedule:
         return "\n".join(lines)
 
 
+# -- inspection steps on the GPU, same signatures as reference inspector.py:185-418 --
+
+def partition_seed(space: IterationSpace, ts: int) -> tuple[TilingFunction, list[Tile]]:
+    """Chunk the seed space into tiles of ts iterations per region (``inspector.py:185-205``)."""
+    from . import _lib
+    if ts < 1:
+        raise ValueError(f"tile size must be >= 1, got {ts}")
+    assignment, m, k = _lib.partition_seed(space, ts)
+    tiles = [Tile(id=i, region=Region.CORE) for i in range(m)]
+    tiles += [Tile(id=m + j, region=Region.BOUNDARY) for j in range(k)]
+    tiles.append(Tile(id=m + k, region=Region.NONEXEC))
+    return TilingFunction(loop_index=0, assignment=assignment), tiles
+
+
+def assign(sigma: TilingFunction, tiles: list[Tile]) -> None:
+    """Per-tile ascending iteration lists by a stable GPU sort (``inspector.py:385-391``)."""
+    from . import _lib
+    off, el = _lib.assign(sigma.assignment, len(tiles))
+    for t in tiles:
+        t.iteration_lists[sigma.loop_index] = el[off[t.id]:off[t.id + 1]].copy()
+
+
+def _seed_adjacency(tiles: list[Tile], seed_map: MeshMap | None) -> dict[int, set[int]]:
+    """Tiles are adjacent iff their seed iterations share a target (``inspector.py:208-225``)."""
+    from . import _lib
+    adjacency: dict[int, set[int]] = {t.id: set() for t in tiles}
+    if seed_map is None:
+        return adjacency
+    sigma0 = np.full(seed_map.source.total, NO_TILE, dtype=np.int64)
+    for t in tiles:
+        lst = t.iteration_lists.get(0)
+        if lst is not None and len(lst):
+            sigma0[lst] = t.id
+    for a, b in _lib.seed_adjacency(seed_map, sigma0, len(tiles)):
+        adjacency[a].add(b)
+        adjacency[b].add(a)
+    return adjacency
+
+
+def color_tiles(tiles: list[Tile], seed_map: MeshMap | None,
+                fake_connections: set[tuple[int, int]], mode: ExecMode,
+                adjacency: dict[int, set[int]] | None = None) -> None:
+    """Greedy first-fit colouring per region (SHARED) or colour = id (``inspector.py:228-263``)."""
+    from . import _lib
+    if mode is ExecMode.SHARED:
+        if adjacency is None:
+            adjacency = _seed_adjacency(tiles, seed_map)
+        pos = {t.id: i for i, t in enumerate(tiles)}
+        pairs = {(min(pos[a], pos[b]), max(pos[a], pos[b]))
+                 for a, nbrs in adjacency.items() for b in nbrs if a in pos and b in pos}
+        pairs |= {(min(pos[a], pos[b]), max(pos[a], pos[b])) for a, b in fake_connections}
+        colors = _lib.color_tiles([int(t.region) for t in tiles], mode.code, sorted(pairs))
+        for t, c in zip(tiles, colors.tolist()):
+            t.color = c
+    else:
+        for t in tiles:
+            t.color = t.id
+
+
+def project(loop, sigma: TilingFunction, phi: dict, conflicts: ConflictMatrix,
+            tiles: list[Tile], inverse_maps: dict | None = None) -> None:
+    """Fold the loop's tiling into the per-space projections on the GPU
+    (``inspector.py:266-316``); ``inverse_maps`` is accepted for signature parity
+    (inverses are built on the device)."""
+    from . import _lib
+    colors = np.array([t.color for t in tiles], dtype=np.int64)
+    arrays = {name: p.assignment for name, p in phi.items()}
+    for a, b in _lib.project(loop, sigma.assignment, colors, arrays):
+        conflicts.add(a, b)
+    spaces = {loop.space.name: loop.space}
+    for d in loop.descriptors:
+        if d.map is not None:
+            spaces[d.map.target.name] = d.map.target
+    for name in spaces:
+        if name in arrays and (name not in phi or arrays[name] is not phi[name].assignment):
+            phi[name] = Projection(spaces[name], arrays[name])
+
+
+def tile_loop(loop, phi: dict, tiles: list[Tile],
+              conflicts: ConflictMatrix | None = None) -> TilingFunction:
+    """Max-colour tiling of a loop from the projections (``inspector.py:319-382``)."""
+    from . import _lib
+    colors = np.array([t.color for t in tiles], dtype=np.int64)
+    arrays = {name: p.assignment for name, p in phi.items()}
+    assignment, pairs = _lib.tile_loop(loop, colors, arrays, conflicts is not None)
+    if conflicts is not None:
+        for a, b in pairs:
+            conflicts.add(a, b)
+    return TilingFunction(loop_index=loop.index, assignment=assignment)
+
+
+def compute_local_maps(tiles: list[Tile], chain: LoopChain) -> None:
+    """Map rows restricted to each tile's list, in list order (``inspector.py:397-418``)."""
+    from . import _lib
+    for t in tiles:
+        t.local_maps.clear()
+    empty = np.empty(0, dtype=np.int64)
+    for j, loop in enumerate(chain.loops):
+        done = []
+        for d in loop.descriptors:
+            if d.is_direct or d.map.name in done:
+                continue
+            done.append(d.map.name)
+            lists = [t.iteration_lists.get(j, empty) for t in tiles]
+            flat = _lib.gather_rows(d.map, np.concatenate(lists) if lists else empty)
+            offset = 0
+            for t, lst in zip(tiles, lists):
+                span = len(lst) * d.map.arity
+                t.local_maps[(j, d.map.name)] = flat[offset:offset + span].copy()
+                offset += span
+
+
 def find_seed_map(chain: LoopChain) -> MeshMap | None:
     """The map used for tile adjacency (reference ``inspector.py:421-430``)."""
     seed_space = chain.loops[0].space
