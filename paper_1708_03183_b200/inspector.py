@@ -251,6 +251,30 @@ class Schedule:
                              ",".join(map(str, t.local_maps[(j, name)].tolist())))
         return ("\n".join(lines) + "\n").encode()
 
+    @classmethod
+    def deserialize(cls, data: bytes) -> "Schedule":
+        """Parse ``schedule-v1`` bytes (the on-disk inspection cache format)."""
+        lines = data.decode().split("\n")
+        if not lines or lines[0] != "schedule-v1":
+            raise ValueError("not a schedule-v1 document")
+        head = dict(ln.split("=", 1) for ln in lines[1:6])
+        tiles = []
+        for ln in lines[6:]:
+            if ln.startswith("tile "):
+                kv = dict(x.split("=") for x in ln.split()[1:])
+                tiles.append(Tile(int(kv["id"]), Region[kv["region"].upper()], int(kv["color"])))
+            elif ln.startswith("  list "):
+                key, _, vals = ln[7:].partition("=")
+                tiles[-1].iteration_lists[int(key)] = np.array(
+                    [int(v) for v in vals.split(",")] if vals else [], dtype=np.int64)
+            elif ln.startswith("  lmap "):
+                key, _, vals = ln[7:].partition("=")
+                j, name = key.split(" ", 1)
+                tiles[-1].local_maps[(int(j), name)] = np.array(
+                    [int(v) for v in vals.split(",")] if vals else [], dtype=np.int64)
+        return cls(ExecMode.parse(head["mode"]), head["fingerprint"], int(head["loops"]), tiles,
+                   int(head["rounds"]))
+
     def summary(self) -> str:
         by_region = {r: len(self.tiles_in_region(r)) for r in Region}
         lines = [
