@@ -20,6 +20,7 @@
 
 #include "lt_dg.cuh"
 #include "lt_kernels.cuh"
+#include "lt_pairs.cuh"
 
 namespace lt {
 
@@ -846,6 +847,8 @@ struct ExecPlan {
   std::vector<DevBuf<uint8_t>> wflags;        // per staged dataset
   StagedParams sp;
   DevBuf<int32_t> region;
+  std::vector<int32_t> rank;  // execution order key: colour refined by write-conflict sub-colour
+  int max_subcolor = 0;
   DevBuf<int32_t> blob, blob_len;
   DevBuf<int64_t> blob_off;
   size_t data_max = 0;  // largest per-tile dataset rows (bytes)
@@ -1108,7 +1111,7 @@ static void build_dependencies(Ctx &ctx, lt_schedule *s, ExecPlan &P) {
     for (int t = 0; t < s->n_tiles; ++t)
       if (s->region[t] == reg) v.push_back(t);
     std::stable_sort(v.begin(), v.end(),
-                     [&](int a, int b) { return s->color[a] < s->color[b]; });
+                     [&](int a, int b) { return P.rank[a] < P.rank[b]; });
     (reg == LT_CORE ? core : bnd) = v;
     all.insert(all.end(), v.begin(), v.end());
   }
@@ -1192,7 +1195,7 @@ static void build_dependencies(Ctx &ctx, lt_schedule *s, ExecPlan &P) {
     U = last_plus(ctx, idx.get(), heads.get(), total);
   }
   DevBuf<int32_t> color(s->n_tiles, ctx.stream);
-  LT_CK(cudaMemcpyAsync(color.get(), s->color.data(), 4 * s->n_tiles, cudaMemcpyHostToDevice,
+  LT_CK(cudaMemcpyAsync(color.get(), P.rank.data(), 4 * s->n_tiles, cudaMemcpyHostToDevice,
                         ctx.stream));
   P.nbr.alloc(std::max<int64_t>(U, 1), ctx.stream);
   DevBuf<uint32_t> owner(std::max<int64_t>(U, 1), ctx.stream);
@@ -1472,6 +1475,107 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   return blob_max;
 }
 
+// ---- same-colour write conflicts -----------------------------------------------------
+// Equal-coloured tiles must not share an element one of them writes.  The
+// inspector guarantees it for complete chains, but the reference algorithm can
+// emit schedules that break it (e.g. FIG2's sub-chain [edge_inc, cell_inc]:
+// reductions of the last loop split over equal-coloured tiles -- 43 violations
+// of the reference's own legality oracle; its sequential executor masks them).
+// Such tiles are ordered into sub-colours in tile-id order, the reference's
+// sequential order, so results stay bitwise equal to execute_schedule.
+__global__ void k_conflict_keys(const int32_t *elem, const uint32_t *tile, int64_t n,
+                                uint64_t flag, uint64_t *keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((uint64_t)(uint32_t)elem[i] << 32) | ((uint64_t)tile[i] << 1) | flag;
+}
+
+__global__ void k_conflict_pairs(const uint64_t *keys, int64_t n, const int32_t *color,
+                                 PairSet ps) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !(keys[i] & 1)) return;
+  const uint64_t e = keys[i] >> 32;
+  const int ti = (int)((keys[i] >> 1) & 0x7fffffff);
+  for (int64_t j = i - 1; j >= 0 && (keys[j] >> 32) == e; --j) {
+    const int tj = (int)((keys[j] >> 1) & 0x7fffffff);
+    if (tj != ti && color[tj] == color[ti]) pair_insert(ps, ti, tj);
+  }
+  for (int64_t j = i + 1; j < n && (keys[j] >> 32) == e; ++j) {
+    const int tj = (int)((keys[j] >> 1) & 0x7fffffff);
+    if (tj != ti && color[tj] == color[ti]) pair_insert(ps, ti, tj);
+  }
+}
+
+static void build_ranks(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPlan &P) {
+  const int nt = s->n_tiles;
+  DevBuf<int32_t> region(nt, ctx.stream), color(nt, ctx.stream);
+  LT_CK(cudaMemcpyAsync(region.get(), s->region.data(), 4 * nt, cudaMemcpyHostToDevice, ctx.stream));
+  LT_CK(cudaMemcpyAsync(color.get(), s->color.data(), 4 * nt, cudaMemcpyHostToDevice, ctx.stream));
+  std::map<int, std::vector<FpSource>> all, wr;
+  for (int j = 0; j < s->n_loops; ++j) {
+    const LoopDesc &L = cv.loops[j];
+    std::vector<int> seen;
+    bool direct = false, direct_w = false;
+    for (const lt_desc &d : L.desc) {
+      const bool w = d.mode != LT_READ;
+      if (d.map < 0) {
+        direct = true;
+        direct_w |= w;
+      } else {
+        if (std::find(seen.begin(), seen.end(), d.map) == seen.end()) {
+          seen.push_back(d.map);
+          all[cv.maps[d.map].target].push_back({j, d.map});
+        }
+        if (w) wr[cv.maps[d.map].target].push_back({j, d.map});
+      }
+    }
+    if (direct) all[L.space].push_back({j, -1});
+    if (direct_w) wr[L.space].push_back({j, -1});
+  }
+  PairTable pt(ctx, pow2_at_least(int64_t(nt) * 16));
+  for (;;) {
+    for (auto &kv : wr) {
+      Footprint fa, fw;
+      build_footprint(ctx, s, cv, all[kv.first], region, fa);
+      build_footprint(ctx, s, cv, kv.second, region, fw);
+      const int64_t n = fa.n + fw.n;
+      if (fw.n == 0) continue;
+      DevBuf<uint64_t> k(n, ctx.stream), ks(n, ctx.stream);
+      if (fa.n)
+        k_conflict_keys<<<grid_for(fa.n, 256), 256, 0, ctx.stream>>>(fa.elem.get(), fa.tile.get(),
+                                                                    fa.n, 0, k.get());
+      k_conflict_keys<<<grid_for(fw.n, 256), 256, 0, ctx.stream>>>(fw.elem.get(), fw.tile.get(),
+                                                                  fw.n, 1, k.get() + fa.n);
+      LT_CK_LAUNCH();
+      size_t tmp = 0;
+      LT_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k.get(), ks.get(), (int)n, 0, 64,
+                                           ctx.stream));
+      DevBuf<char> tb((int64_t)tmp, ctx.stream);
+      LT_CK(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k.get(), ks.get(), (int)n, 0, 64,
+                                           ctx.stream));
+      k_conflict_pairs<<<grid_for(n, 256), 256, 0, ctx.stream>>>(ks.get(), n, color.get(),
+                                                                 pt.view());
+      LT_CK_LAUNCH();
+    }
+    if (pt.status().second) { pt.resize(pt.cap * 2); continue; }
+    break;
+  }
+  std::vector<std::vector<int>> lower(nt);  // conflicting tiles with a smaller id
+  for (unsigned long long key : pt.fetch()) {
+    const int a = (int)(key >> 32), b = (int)(key & 0xffffffffu);
+    lower[std::max(a, b)].push_back(std::min(a, b));
+  }
+  std::vector<int32_t> sub(nt, 0);
+  int max_sub = 0;
+  for (int t = 0; t < nt; ++t)
+    for (int u : lower[t]) {
+      sub[t] = std::max(sub[t], sub[u] + 1);
+      max_sub = std::max(max_sub, (int)sub[t]);
+    }
+  P.max_subcolor = max_sub;
+  P.rank.resize(nt);
+  for (int t = 0; t < nt; ++t) P.rank[t] = s->color[t] * (max_sub + 1) + sub[t];
+}
+
 // Which executor: LT_EXEC=global (tiles read global memory, one launch per
 // colour), staged (footprints in shared memory, one launch per colour) or
 // dataflow (staged, one persistent launch with tile dependencies).  Default:
@@ -1555,6 +1659,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
   const int nl = s->n_loops;
   P.loops.resize(nl);
   P.host_loops.resize(nl);
+  build_ranks(ctx, s, cv, P);
   std::vector<int> ds_of, ds_space, ds_vpe;
   std::vector<double *> ds_ptr;
   size_t regions_max = 0;
@@ -1738,7 +1843,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
   for (int reg : {LT_CORE, LT_BOUNDARY}) {
     std::map<int, std::vector<int32_t>> by_color;
     for (int t = 0; t < s->n_tiles; ++t)
-      if (s->region[t] == reg) by_color[s->color[t]].push_back(t);
+      if (s->region[t] == reg) by_color[P.rank[t]].push_back(t);
     for (auto &kv : by_color) {
       DevBuf<int32_t> ids((int64_t)kv.second.size(), ctx.stream);
       LT_CK(cudaMemcpyAsync(ids.get(), kv.second.data(), sizeof(int32_t) * kv.second.size(),

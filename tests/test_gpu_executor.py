@@ -142,3 +142,21 @@ def test_gpu_nonexec_tile_never_runs():
         # elements whose inputs depend on non-exec data fall into T_ne and keep values
         tne = s.tiles[-1]
         assert np.all(d2["out"].numpy()[tne.iteration_lists[1]] == -7.0)
+
+
+@pytest.mark.parametrize("ts", [2, 4, 8])
+def test_gpu_executes_illegal_reference_schedule_correctly(ts):
+    """The reference inspector emits, for FIG2's sub-chain [edge_inc, cell_inc],
+    schedules whose last-loop reductions split across equal-coloured tiles
+    (violations of its own legality oracle).  The executor orders such tiles
+    (write-conflict sub-colours in id order) and matches the sequential result."""
+    mesh, (chain, data, vpe, bind) = build_case("fig2", (16, 8), "rcm")
+    sub = chain.subchain(0, 2)
+    sched = lt.inspect_chain(sub, ts, lt.ExecMode.SHARED)
+    ds = {n: lt.Dataset(n, chain.space_named(_space_of(chain, bind, n)), vpe[n], v)
+          for n, v in data.items()}
+    lt.execute_schedule(sched, sub, bind[:2], ds, lt.default_registry())
+    ref = {n: v.copy() for n, v in data.items()}
+    O.execute_untiled(sub, bind[:2], ref, vpe)
+    for n in ref:
+        np.testing.assert_array_equal(ds[n].numpy(), ref[n], err_msg=n)
