@@ -510,8 +510,15 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
   __shared__ int item;
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   unsigned phase = 0;
+  // the next queue item is popped one tile ahead, hiding the atomic's latency;
+  // a CTA still runs its items in queue order, so waits only target items
+  // held by running CTAs and the schedule stays deadlock-free
+  int next = threadIdx.x == 0 ? atomicAdd(D.queue, 1) : 0;
   for (;;) {
-    if (threadIdx.x == 0) item = atomicAdd(D.queue, 1);
+    if (threadIdx.x == 0) {
+      item = next;
+      next = atomicAdd(D.queue, 1);
+    }
     __syncthreads();
     const int it = item;
     if (it >= D.n_items) return;
@@ -521,13 +528,14 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     phase ^= 1u;
     const int n0 = D.nbr_off[t], n1 = D.nbr_off[t + 1];
     LT_TSTAMP(t_wait);
+    // ld.acquire.gpu also invalidates this SM's L1 (CCTL.IVALL), so the
+    // gathers below cannot see stale lines of rows other tiles wrote
     for (int i = n0 + threadIdx.x; i < n1; i += LT_SBLOCK) {
       const int e = D.nbr[i];
       const int need = k + (e & 1);
       const int32_t *flag = D.done + (e >> 1);
       while (ld_acquire(flag) < need) __nanosleep(32);
     }
-    __threadfence();  // gpu-scope fence: drop stale L1 lines before gathering
     __syncthreads();
     LT_TACC(3, t_wait);
     LT_TSTAMP(t_tile);
@@ -535,10 +543,9 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     // release: barrier, then one cumulative gpu-scope fence + increment
     // (the arrive pattern of CUTLASS's GenericBarrier)
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(D.done + t, 1);
-    }
+    if (threadIdx.x == 0)
+      asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(D.done + t)
+                   : "memory");
     LT_TACC(4, t_tile);
 #ifdef LT_PHASE_TIMING
     if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[5], 1ull);
@@ -1038,6 +1045,12 @@ static std::string plan_key(const ChainView &cv, const lt_arg *args, int use_loc
 }
 
 static const size_t kSmemBudget = 96 * 1024;
+// shared scratch for one chunk of INC contributions in the staged executor
+// (smaller chunks: more apply phases, more resident tiles per SM)
+static size_t scratch_budget() {
+  const char *e = getenv("LT_SCRATCH_KB");
+  return (e ? (size_t)atoi(e) : 24) * 1024;
+}
 static std::string g_last_fit;
 static const size_t kSmemMax = 227 * 1024;
 
@@ -1673,7 +1686,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     P.dataflow = P.staged && pref != 1;
   }
   const int block = P.staged ? LT_SBLOCK : LT_BLOCK;
-  const size_t budget = P.staged ? std::min<size_t>(24 * 1024, kSmemMax - regions_max)
+  const size_t budget = P.staged ? std::min<size_t>(scratch_budget(), kSmemMax - regions_max)
                                  : kSmemBudget;
   size_t scratch_max = 0;
   int a = 0;
