@@ -73,6 +73,7 @@ struct TileCtx {
     const DArg &A = L.a[d];
     return smem + A.inc_off + (lpos * A.arity + k) * A.vpe;
   }
+  __device__ double *rec(int k) const { return smem + (lpos * L.a[4].arity + k) * L.rec; }
 };
 
 struct FlatCtx {  // untiled: element ids, global scratch
@@ -91,6 +92,9 @@ struct FlatCtx {  // untiled: element ids, global scratch
   __device__ double *inc(int d, int k) const {
     const DArg &A = L.a[d];
     return A.scr + ((size_t)e * A.arity + k) * A.vpe;
+  }
+  __device__ double *rec(int k) const {
+    return L.a[4].scr + ((size_t)e * L.a[4].arity + k) * L.rec;
   }
 };
 
@@ -120,13 +124,14 @@ struct StagedCtx {
     const DArg &A = L.a[d];
     return scratch + A.inc_off + (lpos * A.arity + k) * A.vpe;
   }
+  __device__ double *rec(int k) const { return scratch + (lpos * L.a[4].arity + k) * L.rec; }
 };
 
 // FAM selects which DG degree is compiled into an instantiation (0: scalar
 // kernels only, 1..4: scalar + DG P, 5: everything) so a P1 chain does not
 // pay the register footprint of P4 bodies.
 template <int FAM, class C>
-__device__ __forceinline__ void dispatch(int kernel, C &c) {
+__device__ __forceinline__ void dispatch(int kernel, C &c, int lane) {
   switch (kernel) {
     case K_EDGE_INC: body_edge_inc(c); break;
     case K_CELL_INC: body_edge_inc(c); break;  // same body: every target += own value
@@ -136,8 +141,39 @@ __device__ __forceinline__ void dispatch(int kernel, C &c) {
     case K_TOY_K2: body_toy_k2(c); break;
     case K_TOY_K3: body_toy_k3(c); break;
     default:
-      if (FAM > 0) dg_dispatch<FAM>(kernel - K_DG_FIRST, c);
+      if (FAM > 0) dg_dispatch<FAM>(kernel - K_DG_FIRST, c, lane);
       break;
+  }
+}
+
+// Deferred apply of DG facet records for one (target, DoF row i): the target's
+// ru/rs row values (du, ds: component i) plus every contributor's lifted record
+// in (element, k) order.
+template <int FAM>
+__device__ __forceinline__ void lift_apply_item(const DLoop &L, double *du, double *ds, int nd,
+                                                int i, const double *recs, const int *slots,
+                                                int s0, int s1) {
+  double acc[5] = {du[0], du[nd], ds[0], ds[nd], ds[2 * nd]};
+  for (int s = s0; s < s1; ++s)
+    dg_lift_acc<FAM>(L.kernel - K_DG_FIRST, L.params, i, recs + (size_t)slots[s] * L.rec, acc);
+  du[0] = acc[0];
+  du[nd] = acc[1];
+  ds[0] = acc[2];
+  ds[nd] = acc[3];
+  ds[2 * nd] = acc[4];
+}
+
+// Work items (element, lane) of cnt elements with `lanes` items each, strided
+// over `step` threads, stepped incrementally (no division per item).
+template <class F>
+__device__ __forceinline__ void for_items(int cnt, int lanes, int step, F &&f) {
+  const int dq = step / lanes, dr = step - dq * lanes;
+  int e = threadIdx.x / lanes, l = threadIdx.x - e * lanes;
+  while (e < cnt) {
+    f(e, l);
+    e += dq;
+    l += dr;
+    if (l >= lanes) { l -= lanes; ++e; }
   }
 }
 
@@ -175,16 +211,27 @@ __global__ void __launch_bounds__(LT_BLOCK) k_fused_tiles(const DLoop *__restric
     if (n == 0) continue;
     const int CH = L.chunk;
     for (int c0 = 0; c0 < n; c0 += CH) {
-      const int lp = threadIdx.x;
-      if (lp < CH && c0 + lp < n) {
+      for_items(min(CH, n - c0), L.lanes, blockDim.x, [&](int lp, int lane) {
         const int gpos = beg + c0 + lp;
         TileCtx cx{L, L.elements[gpos], gpos, lp, smem};
-        dispatch<FAM>(L.kernel, cx);
-      }
+        dispatch<FAM>(L.kernel, cx, lane);
+      });
       if (L.n_inc) {
         __syncthreads();
         const int gc = L.chunk_base[t] + c0 / CH;
-        for (int i = 0; i < L.n_inc; ++i) apply_chunk(L, L.inc[i], gc, smem);
+        if (L.deferred) {
+          const IncPlan &P = L.inc[0];
+          const int nd = L.a[4].vpe >> 1, u0 = P.gc_off[gc];
+          const int work = (P.gc_off[gc + 1] - u0) * nd;
+          for (int w = threadIdx.x; w < work; w += blockDim.x) {
+            const int u = u0 + w / nd, i = w - (w / nd) * nd;
+            lift_apply_item<FAM>(L, L.a[4].data + (size_t)P.utgt[u] * L.a[4].vpe + i,
+                                 L.a[5].data + (size_t)P.utgt[u] * L.a[5].vpe + i, nd, i, smem,
+                                 P.slots, P.ut_off[u], P.ut_off[u + 1]);
+          }
+        } else {
+          for (int i = 0; i < L.n_inc; ++i) apply_chunk(L, L.inc[i], gc, smem);
+        }
         __syncthreads();
       }
     }
@@ -403,6 +450,32 @@ __device__ __forceinline__ void tile_prefetch(const StagedParams &P, int t, doub
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// Deferred apply of a DG facet loop's chunk: one work item per (unique target,
+// DoF row); each contributor's correction record is lifted and added in
+// (element, k) order -- the reference's sequential order -- straight into the
+// target's ru/rs rows in shared memory.
+template <int FAM>
+__device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off, const int *utgt,
+                                               const int *ut_off, const int *slots, int c,
+                                               const double *scratch, double *smem,
+                                               const int *base) {
+  if (FAM == 0) return;
+  const DArg &Au = L.a[4], &As = L.a[5];
+  const int nd = Au.vpe >> 1;
+  double *ru = smem + base[Au.ds], *rs = smem + base[As.ds];
+  const int u0 = gc_off[c], nu = gc_off[c + 1] - u0;
+  const int dq = LT_SBLOCK / nd, dr = LT_SBLOCK - dq * nd;
+  int q = threadIdx.x / nd, i = threadIdx.x - q * nd;
+  while (q < nu) {
+    const int u = u0 + q;
+    lift_apply_item<FAM>(L, ru + utgt[u] * Au.sstride + i, rs + utgt[u] * As.sstride + i, nd, i,
+                         scratch, slots, ut_off[u], ut_off[u + 1]);
+    q += dq;
+    i += dr;
+    if (i >= nd) { i -= nd; ++q; }
+  }
+}
+
 // Phase 2: gather the datasets the chain writes, run every loop on shared
 // memory, store back the rows this tile wrote.
 template <int FAM>
@@ -422,13 +495,37 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     const int n = LH[0];
     if (n == 0) continue;
     LT_TSTAMP(t_loop);
+    if (L.deferred) {  // DG facet loop: records, then lifted ordered apply
+      const int CH = L.chunk;
+      const int *pb = LH + 2 + L.n_desc;
+      for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
+        for_items(min(CH, n - c0), L.lanes, LT_SBLOCK, [&](int lp, int lane) {
+          StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+          dispatch<FAM>(L.kernel, cx, lane);
+        });
+        __syncthreads();
+        apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base);
+        __syncthreads();
+      }
+      LT_TACC(8 + (j < 24 ? j : 23), t_loop);
+      continue;
+    }
+    if (!L.n_inc) {  // direct / mapped-read loop: all items of the list at once
+      for_items(n, L.lanes, LT_SBLOCK, [&](int pos, int lane) {
+        StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+        dispatch<FAM>(L.kernel, cx, lane);
+      });
+      __syncthreads();
+      LT_TACC(8 + (j < 24 ? j : 23), t_loop);
+      continue;
+    }
     const int CH = L.chunk;
     for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
       LT_TSTAMP(t_body);
-      if (tid < CH && c0 + tid < n) {
-        StagedCtx cx{L, 0, c0 + tid, tid, smem, scratch, base, B, LH + 2};
-        dispatch<FAM>(L.kernel, cx);
-      }
+      for_items(min(CH, n - c0), L.lanes, LT_SBLOCK, [&](int lp, int lane) {
+        StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+        dispatch<FAM>(L.kernel, cx, lane);
+      });
       LT_TACC(32 + (j < 4 ? j : 3), t_body);
       if (L.n_inc) {
         __syncthreads();
@@ -556,11 +653,12 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
 // ---- untiled executor --------------------------------------------------------------
 template <int FAM>
 __global__ void __launch_bounds__(256) k_untiled_body(const DLoop *__restrict__ Lp, int n) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
   const DLoop &L = *Lp;
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int e = (int)(w / L.lanes);
+  if (e >= n) return;
   FlatCtx cx{L, e};
-  dispatch<FAM>(L.kernel, cx);
+  dispatch<FAM>(L.kernel, cx, (int)(w - (int64_t)e * L.lanes));
 }
 
 // smallest instantiation covering every kernel of the chain
@@ -586,6 +684,8 @@ static FusedFn fused_fn(int fam) {
     default: return k_fused_tiles<5>;
   }
 }
+typedef void (*DeferredFn)(const DLoop *, const int32_t *, const int32_t *, int64_t, int);
+static DeferredFn untiled_deferred_fn(int fam);
 static UntiledFn untiled_fn(int fam) {
   switch (fam) {
     case 0: return k_untiled_body<0>;
@@ -627,6 +727,33 @@ __global__ void k_untiled_apply(const DLoop *__restrict__ Lp, int d, const int32
   }
 }
 
+// deferred DG facet records: one thread per (target, DoF row)
+template <int FAM>
+__global__ void k_untiled_apply_deferred(const DLoop *__restrict__ Lp, const int32_t *inv_off,
+                                         const int32_t *inv_flat, int64_t n_target,
+                                         int exec_size) {
+  const DLoop &L = *Lp;
+  const int nd = L.a[4].vpe >> 1, ar = L.a[4].arity;
+  int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= n_target * nd) return;
+  const int64_t t = w / nd;
+  const int i = (int)(w - t * nd);
+  int b = inv_off[t], e = inv_off[t + 1];
+  while (e > b && inv_flat[e - 1] / ar >= exec_size) --e;  // ascending: non-exec sources last
+  lift_apply_item<FAM>(L, L.a[4].data + t * L.a[4].vpe + i, L.a[5].data + t * L.a[5].vpe + i, nd,
+                       i, L.a[4].scr, inv_flat, b, e);
+}
+
+static DeferredFn untiled_deferred_fn(int fam) {
+  switch (fam) {
+    case 1: return k_untiled_apply_deferred<1>;
+    case 2: return k_untiled_apply_deferred<2>;
+    case 3: return k_untiled_apply_deferred<3>;
+    case 4: return k_untiled_apply_deferred<4>;
+    default: return k_untiled_apply_deferred<5>;
+  }
+}
+
 // ---- plan building -------------------------------------------------------------------
 __global__ void k_inc_keys(const int32_t *elements, const int32_t *sigma, const int32_t *offsets,
                            const int32_t *chunk_base, const int32_t *map, int arity, int CH,
@@ -665,6 +792,8 @@ __global__ void k_set_int(int32_t *p, int32_t v) { *p = v; }
 
 struct IncBuffers {
   DevBuf<int32_t> gc_off, utgt, ut_off, slots;
+  DevBuf<uint32_t> run_gc;  // global chunk of each unique target
+  int64_t runs = 0;
 };
 
 // ---- tile footprints (staged executor plan) ------------------------------------------
@@ -830,6 +959,7 @@ static void build_footprint(Ctx &ctx, const lt_schedule *s, const ChainView &cv,
 
 struct LoopPlan {
   int chunk = LT_BLOCK;
+  bool deferred = false;    // staged: DG facet loop applied by its deferred lift
   int scratch_per_pos = 0;  // doubles
   DevBuf<int32_t> chunk_base;
   DevBuf<int32_t> gc_tile;  // staged: tile of each global chunk
@@ -919,7 +1049,9 @@ static void build_inc_plan(Ctx &ctx, const lt_schedule *s, int j, const lt_map &
   const int64_t R = (int64_t)last_idx + last_head;
   out.utgt.alloc(R, ctx.stream);
   out.ut_off.alloc(R + 1, ctx.stream);
-  DevBuf<uint32_t> run_gc(R, ctx.stream);
+  out.run_gc.alloc(R, ctx.stream);
+  out.runs = R;
+  DevBuf<uint32_t> &run_gc = out.run_gc;
   k_run_fill<<<grid_for(nnz, 256), 256, 0, ctx.stream>>>(kout.get(), heads.get(), run_idx.get(),
                                                          nnz, out.utgt.get(), out.ut_off.get(),
                                                          run_gc.get());
@@ -1016,6 +1148,11 @@ static void fill_dloop(DLoop &D, const ChainView &cv, int j, const lt_arg *args,
   D.n_desc = (int)L.desc.size();
   D.use_local = use_local;
   D.exec_size = (int)cv.exec_size(L.space);
+  D.lanes = L.kernel >= K_DG_FIRST ? dg_lanes(L.kernel - K_DG_FIRST) : 1;
+  if (L.kernel >= K_DG_FIRST && dg_is_flux(L.kernel - K_DG_FIRST)) {  // validated: one map, INC
+    D.deferred = 1;
+    D.rec = dg_corr_size(L.kernel - K_DG_FIRST);
+  }
   auto it = ctx.params.find(L.kernel);
   D.params = it == ctx.params.end() ? nullptr : it->second.get();
   for (int d = 0; d < D.n_desc; ++d) {
@@ -1419,6 +1556,14 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       h[1] = cb[j].empty() ? 0 : cb[j][t + 1] - cb[j][t];
       const int nd = (int)cv.loops[j].desc.size();
       for (int d = 0; d < nd; ++d) {
+        // descriptors with the same map (or all direct ones) share one slot map
+        int same = -1;
+        for (int e = 0; e < d && same < 0; ++e)
+          if (cv.loops[j].desc[e].map == cv.loops[j].desc[d].map) same = e;
+        if (same >= 0) {
+          h[2 + d] = h[2 + same];
+          continue;
+        }
         const int ar = cv.loops[j].desc[d].map < 0 ? 1 : cv.maps[cv.loops[j].desc[d].map].arity;
         h[2 + d] = put(s_slot[j][d], (int64_t)o * ar, n * ar, 0);
       }
@@ -1702,10 +1847,23 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       spp += D.a[d].arity * D.a[d].vpe;
       LP.inc_desc.push_back(d);
     }
+    // DG facet loops keep per-side correction records (5 NQ + 2 doubles)
+    // instead of lifted increments (5 ND each)
+    LP.deferred = D.deferred;
+    if (D.deferred) spp = D.a[4].arity * D.rec;
     LP.scratch_per_pos = spp;
     LP.chunk = choose_chunk(spp, budget, block);
+    if (spp) {  // no larger than the longest tile list of the loop (scratch is per CTA)
+      std::vector<int32_t> off(s->n_tiles + 1);
+      LT_CK(cudaMemcpyAsync(off.data(), s->lists[j].offsets.get(), 4 * (s->n_tiles + 1),
+                            cudaMemcpyDeviceToHost, ctx.stream));
+      LT_CK(cudaStreamSynchronize(ctx.stream));
+      int longest = 1;
+      for (int t = 0; t < s->n_tiles; ++t) longest = std::max(longest, off[t + 1] - off[t]);
+      LP.chunk = std::min(LP.chunk, longest);
+    }
     for (int d : LP.inc_desc) D.a[d].inc_off *= LP.chunk;
-    scratch_max = std::max(scratch_max, sizeof(double) * (size_t)spp * LP.chunk);
+    scratch_max = std::max(scratch_max, sizeof(double) * (size_t)LP.scratch_per_pos * LP.chunk);
     D.chunk = LP.chunk;
     const LoopLists &Lj = s->lists[j];
     D.offsets = Lj.offsets.get();
@@ -2033,10 +2191,15 @@ static void execute_untiled(Ctx &ctx, const ChainView &cv, const lt_arg *args,
     DLoop &D = host[j];
     fill_dloop(D, cv, (int)j, args + a, ctx, 0);
     const int64_t n = cv.exec_size(L.space);
-    for (int d = 0; d < D.n_desc; ++d) {
-      if (L.desc[d].map < 0 || L.desc[d].mode == LT_READ) continue;
-      scratch.emplace_back(std::max<int64_t>(n * D.a[d].arity * D.a[d].vpe, 1), ctx.stream);
-      D.a[d].scr = scratch.back().get();
+    if (D.deferred) {  // one correction record per (element, k)
+      scratch.emplace_back(std::max<int64_t>(n * D.a[4].arity * D.rec, 1), ctx.stream);
+      D.a[4].scr = scratch.back().get();
+    } else {
+      for (int d = 0; d < D.n_desc; ++d) {
+        if (L.desc[d].map < 0 || L.desc[d].mode == LT_READ) continue;
+        scratch.emplace_back(std::max<int64_t>(n * D.a[d].arity * D.a[d].vpe, 1), ctx.stream);
+        D.a[d].scr = scratch.back().get();
+      }
     }
     a += D.n_desc;
   }
@@ -2048,9 +2211,22 @@ static void execute_untiled(Ctx &ctx, const ChainView &cv, const lt_arg *args,
     const int64_t n = cv.exec_size(L.space);
     visits += n;
     if (n == 0) continue;
-    ufn<<<grid_for(n, 256), 256, 0, ctx.stream>>>(dl.get() + j, (int)n);
+    ufn<<<grid_for(n * host[j].lanes, 256), 256, 0, ctx.stream>>>(dl.get() + j, (int)n);
     LT_CK_LAUNCH();
     ++launches;
+    if (host[j].deferred) {
+      const lt_map &mp = cv.maps[L.desc[4].map];
+      const int64_t nt = cv.total(mp.target);
+      InvVal &inv = cached_inverse(ctx, mp, cv.total(mp.source), nt);
+      const int64_t work = nt * (host[j].a[4].vpe >> 1);
+      if (work) {
+        untiled_deferred_fn(chain_family(cv))<<<grid_for(work, 256), 256, 0, ctx.stream>>>(
+            dl.get() + j, inv.off.get(), inv.flat.get(), nt, (int)n);
+        LT_CK_LAUNCH();
+        ++launches;
+      }
+      continue;
+    }
     for (int d = 0; d < (int)L.desc.size(); ++d) {
       if (L.desc[d].map < 0 || L.desc[d].mode == LT_READ) continue;
       const lt_map &mp = cv.maps[L.desc[d].map];

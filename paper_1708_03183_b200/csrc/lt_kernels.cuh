@@ -7,6 +7,8 @@
 //   C::wr(d)      double*       of the element's own values      (direct W/RW)
 //   C::rdm(d, k)  const double* of the k-th mapped target         (mapped READ)
 //   C::inc(d, k)  double*       contribution slot for target k    (mapped INC / WRITE)
+// Bodies are called once per (element, lane), lane < the kernel's lanes
+// (scalar bodies: 1 lane); lanes of an element write disjoint outputs.
 // Mapped INC/WRITE bodies never touch the target itself: they fill their
 // contribution slot and the executor applies the slots in the reference's
 // sequential order (element ascending, then k) -- no atomics anywhere.
@@ -51,7 +53,9 @@ struct DArg {
 };
 
 #define LT_MAX_STAGED 16  // distinct datasets staged in shared memory
+#ifndef LT_SBLOCK
 #define LT_SBLOCK 128     // threads per CTA of the staged tile executor
+#endif
 
 // One dataset staged in shared memory: the tile's footprint rows of it are
 // gathered at tile start and the rows the tile wrote are stored back at the end.
@@ -85,7 +89,9 @@ struct DLoop {
   int32_t use_local;
   int32_t exec_size;
   int32_t n_plans;          // staged: distinct ordered-gather plans (maps) of the loop
-  int32_t pad2;
+  int32_t deferred;         // staged: INC applied by the kernel's deferred (lifting) apply
+  int32_t lanes;            // work items (lanes) per element
+  int32_t rec;              // deferred: doubles per (element, k) record in the scratch
   const double *params;
   const int32_t *offsets;   // tiled: per-tile list offsets
   const int32_t *elements;  // tiled: concatenated lists
