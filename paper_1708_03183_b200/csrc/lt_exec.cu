@@ -177,6 +177,19 @@ __device__ __forceinline__ void for_items(int cnt, int lanes, int step, F &&f) {
   }
 }
 
+// same over LT_SBLOCK threads with the loop's precomputed stepping constants
+template <class F>
+__device__ __forceinline__ void for_items_s(int cnt, const DLoop &L, F &&f) {
+  const int lanes = L.lanes;
+  int e = lt_div(threadIdx.x, lanes, L.lane_magic), l = threadIdx.x - e * lanes;
+  while (e < cnt) {
+    f(e, l);
+    e += L.lane_dq;
+    l += L.lane_dr;
+    if (l >= lanes) { l -= lanes; ++e; }
+  }
+}
+
 // ---- fused tiled executor ------------------------------------------------------
 __device__ __forceinline__ void apply_chunk(const DLoop &L, const IncPlan &P, int gc,
                                             const double *smem) {
@@ -413,12 +426,11 @@ __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, doub
   const int nrow = B[2 * S.sp];
   const int *idx = B + B[2 * S.sp + 1];
   const double *src = S.data;
-  const int di = LT_SBLOCK / v, dc = LT_SBLOCK - di * v;
-  int i = threadIdx.x / v, c = threadIdx.x - i * v;
+  int i = lt_div(threadIdx.x, v, S.magic), c = threadIdx.x - i * v;
   while (i < nrow) {
-    cp_async8(rows + i * sv + c, src + (size_t)idx[i] * v + c);
-    i += di;
-    c += dc;
+    cp_async8(rows + i * sv + c, src + ((uint32_t)idx[i] * (uint32_t)v + (uint32_t)c));
+    i += S.di;
+    c += S.dc;
     if (c >= v) { c -= v; ++i; }
   }
 }
@@ -464,14 +476,13 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
   const int nd = Au.vpe >> 1;
   double *ru = smem + base[Au.ds], *rs = smem + base[As.ds];
   const int u0 = gc_off[c], nu = gc_off[c + 1] - u0;
-  const int dq = LT_SBLOCK / nd, dr = LT_SBLOCK - dq * nd;
-  int q = threadIdx.x / nd, i = threadIdx.x - q * nd;
+  int q = lt_div(threadIdx.x, nd, L.row_magic), i = threadIdx.x - q * nd;
   while (q < nu) {
     const int u = u0 + q;
     lift_apply_item<FAM>(L, ru + utgt[u] * Au.sstride + i, rs + utgt[u] * As.sstride + i, nd, i,
                          scratch, slots, ut_off[u], ut_off[u + 1]);
-    q += dq;
-    i += dr;
+    q += L.row_dq;
+    i += L.row_dr;
     if (i >= nd) { i -= nd; ++q; }
   }
 }
@@ -499,7 +510,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       const int CH = L.chunk;
       const int *pb = LH + 2 + L.n_desc;
       for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
-        for_items(min(CH, n - c0), L.lanes, LT_SBLOCK, [&](int lp, int lane) {
+        for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
           StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
           dispatch<FAM>(L.kernel, cx, lane);
         });
@@ -511,7 +522,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       continue;
     }
     if (!L.n_inc) {  // direct / mapped-read loop: all items of the list at once
-      for_items(n, L.lanes, LT_SBLOCK, [&](int pos, int lane) {
+      for_items_s(n, L, [&](int pos, int lane) {
         StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
         dispatch<FAM>(L.kernel, cx, lane);
       });
@@ -522,7 +533,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     const int CH = L.chunk;
     for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
       LT_TSTAMP(t_body);
-      for_items(min(CH, n - c0), L.lanes, LT_SBLOCK, [&](int lp, int lane) {
+      for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
         StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
         dispatch<FAM>(L.kernel, cx, lane);
       });
@@ -550,12 +561,11 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     const int *flag = B + B[P.ds_pos + d];
     double *dst = S.data;
     const double *rows = smem + base[d];
-    const int di = LT_SBLOCK / v, dc = LT_SBLOCK - di * v;
-    int i = tid / v, c = tid - i * v;
+    int i = lt_div(tid, v, S.magic), c = tid - i * v;
     while (i < nrow) {
-      if (flag[i]) dst[(size_t)idx[i] * v + c] = rows[i * sv + c];
-      i += di;
-      c += dc;
+      if (flag[i]) dst[(uint32_t)idx[i] * (uint32_t)v + (uint32_t)c] = rows[i * sv + c];
+      i += S.di;
+      c += S.dc;
       if (c >= v) { c -= v; ++i; }
     }
   }
@@ -1149,9 +1159,16 @@ static void fill_dloop(DLoop &D, const ChainView &cv, int j, const lt_arg *args,
   D.use_local = use_local;
   D.exec_size = (int)cv.exec_size(L.space);
   D.lanes = L.kernel >= K_DG_FIRST ? dg_lanes(L.kernel - K_DG_FIRST) : 1;
+  D.lane_magic = lt_magic(D.lanes);
+  D.lane_dq = LT_SBLOCK / D.lanes;
+  D.lane_dr = LT_SBLOCK % D.lanes;
   if (L.kernel >= K_DG_FIRST && dg_is_flux(L.kernel - K_DG_FIRST)) {  // validated: one map, INC
     D.deferred = 1;
     D.rec = dg_corr_size(L.kernel - K_DG_FIRST);
+    const int nd = dg_nd((L.kernel - K_DG_FIRST) / 5 + 1);
+    D.row_magic = lt_magic(nd);
+    D.row_dq = LT_SBLOCK / nd;
+    D.row_dr = LT_SBLOCK % nd;
   }
   auto it = ctx.params.find(L.kernel);
   D.params = it == ctx.params.end() ? nullptr : it->second.get();
@@ -1793,6 +1810,8 @@ static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_
     if (direct) sources[cv.loops[j].space].push_back({j, -1});
   }
   if (sources.size() > LT_MAX_SPACES) return false;
+  for (size_t k = 0; k < ds_ptr.size(); ++k)  // 32-bit row offsets in the gather/store-back
+    if ((uint64_t)cv.total(ds_space[k]) * (uint64_t)ds_vpe[k] >= (1ull << 32)) return false;
   for (auto &kv : sources) build_footprint(ctx, s, cv, kv.second, P.region, P.fp[kv.first]);
   // shared-memory regions of the largest tile: footprint ids + dataset rows
   regions_max = 0;
@@ -1962,6 +1981,9 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       H.ds[k].data = ds_ptr[k];
       H.ds[k].vpe = ds_vpe[k];
       H.ds[k].stride = ds_vpe[k] | 1;
+      H.ds[k].di = LT_SBLOCK / ds_vpe[k];
+      H.ds[k].dc = LT_SBLOCK % ds_vpe[k];
+      H.ds[k].magic = lt_magic(ds_vpe[k]);
       H.ds[k].sp = sp_index.at(ds_space[k]);
       H.ds[k].load = 1;
       H.ds[k].ro = 1;

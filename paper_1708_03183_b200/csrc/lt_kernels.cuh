@@ -70,7 +70,19 @@ struct StageDS {
   int32_t load;            // 0: every footprint row is written before it is read
   int32_t written;         // the tile writes some rows of it (store-back flags present)
   int32_t ro;              // never written by the chain: gathered before dependency waits
+  // flattened (row, component) stepping over LT_SBLOCK threads, no runtime division
+  int32_t di, dc;          // LT_SBLOCK / vpe, LT_SBLOCK % vpe
+  uint32_t magic;          // x / vpe == umulhi(x, magic) for x < 2^16 (vpe >= 2)
+  int32_t pad;
 };
+
+// x / d for 0 <= x < 2^16, 1 <= d < 256, with magic = 2^32 / d + 1 (host: lt_magic)
+__host__ __device__ __forceinline__ uint32_t lt_magic(int d) {
+  return d > 1 ? (uint32_t)((1ull << 32) / (unsigned)d + 1) : 0u;
+}
+__device__ __forceinline__ int lt_div(int x, int d, uint32_t magic) {
+  return d == 1 ? x : (int)__umulhi((unsigned)x, magic);
+}
 
 struct IncPlan {
   int32_t desc;
@@ -92,6 +104,11 @@ struct DLoop {
   int32_t deferred;         // staged: INC applied by the kernel's deferred (lifting) apply
   int32_t lanes;            // work items (lanes) per element
   int32_t rec;              // deferred: doubles per (element, k) record in the scratch
+  uint32_t lane_magic;      // lt_magic(lanes)
+  int32_t lane_dq, lane_dr; // LT_SBLOCK / lanes, LT_SBLOCK % lanes
+  uint32_t row_magic;       // deferred apply: lt_magic(rows per target)
+  int32_t row_dq, row_dr;   // LT_SBLOCK / rows, LT_SBLOCK % rows
+  int32_t pad4;
   const double *params;
   const int32_t *offsets;   // tiled: per-tile list offsets
   const int32_t *elements;  // tiled: concatenated lists
