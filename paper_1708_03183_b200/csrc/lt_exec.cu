@@ -325,7 +325,7 @@ __device__ unsigned long long g_phase_cycles[40];
 struct StagedParams {
   int32_t n_loops, n_ds, n_sp, hs;   // hs: header ints
   int32_t loop_pos[LT_MAX_SLOOPS];   // header position of each loop's block
-  int32_t ds_pos;                    // header position of the written-flag bases
+  int32_t ds_pos;                    // header position of the written-row lists
   int32_t pad;
   const int32_t *blob;
   const int64_t *blob_off;           // per tile: first int of its blob
@@ -558,12 +558,14 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     const int v = S.vpe, sv = S.stride;
     const int nrow = B[2 * S.sp];
     const int *idx = B + B[2 * S.sp + 1];
-    const int *flag = B + B[P.ds_pos + d];
+    const int nw = B[P.ds_pos + 2 * d];          // rows this tile wrote
+    const int *wl = B + B[P.ds_pos + 2 * d + 1];  // their footprint positions
     double *dst = S.data;
     const double *rows = smem + base[d];
     int i = lt_div(tid, v, S.magic), c = tid - i * v;
-    while (i < nrow) {
-      if (flag[i]) dst[(uint32_t)idx[i] * (uint32_t)v + (uint32_t)c] = rows[i * sv + c];
+    while (i < nw) {
+      const int r = wl[i];
+      dst[(uint32_t)idx[r] * (uint32_t)v + (uint32_t)c] = rows[r * sv + c];
       i += S.di;
       c += S.dc;
       if (c >= v) { c -= v; ++i; }
@@ -992,6 +994,8 @@ struct ExecPlan {
   // staged
   std::map<int, Footprint> fp;               // per space
   std::vector<DevBuf<uint8_t>> wflags;        // per staged dataset
+  std::vector<DevBuf<int32_t>> wlist;         // per dataset: written footprint positions
+  std::vector<std::vector<int32_t>> wbeg;     // per dataset, per tile: first entry in wlist
   StagedParams sp;
   DevBuf<int32_t> region;
   std::vector<int32_t> rank;  // execution order key: colour refined by write-conflict sub-colour
@@ -1480,6 +1484,22 @@ static void build_runs(Ctx &ctx, const Footprint &fp, const uint8_t *flag, int n
   LT_CK(cudaStreamSynchronize(ctx.stream));
 }
 
+__global__ void k_u8_to_i32(const uint8_t *a, int64_t n, int32_t *b) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+
+__global__ void k_compact_written(const uint8_t *flag, const int32_t *scan, const uint32_t *tile,
+                                  const int32_t *fp_off, int64_t n, int32_t *out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) out[scan[i]] = (int32_t)(i - fp_off[tile[i]]);
+}
+
+__global__ void k_gather_at(const int32_t *src, const int32_t *idx, int64_t n, int32_t *out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = src[idx[i]];
+}
+
 // Lay out and fill the per-tile programs; returns the largest blob in bytes.
 static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPlan &P,
                           const std::map<int, int> &sp_index, const std::vector<int> &ds_space) {
@@ -1492,7 +1512,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
     hp += 2 + (int)cv.loops[j].desc.size() + 4 * (int)P.loops[j].plan_map.size();
   }
   H.ds_pos = hp;
-  hp += H.n_ds;
+  hp += 2 * H.n_ds;
   H.hs = hp;
   // host copies of the per-tile ranges
   std::vector<std::vector<int32_t>> off(nl), cb(nl);
@@ -1542,7 +1562,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
     }
   }
   for (int k = 0; k < H.n_ds; ++k)
-    if (P.wflags[k].get()) s_wf[k] = (int)secs.size(), sec(P.wflags[k].get(), true);
+    if (P.wflags[k].get()) s_wf[k] = (int)secs.size(), sec(P.wlist[k].get(), false);
   std::vector<int32_t> hdr(H.hs);
   int n_exec = 0;
   for (int t = 0; t < nt; ++t) {
@@ -1597,10 +1617,11 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       }
     }
     for (int k = 0; k < H.n_ds; ++k) {
+      hdr[H.ds_pos + 2 * k] = 0;
       if (s_wf[k] < 0) continue;
-      const int sp = H.ds[k].sp;
-      const int32_t o = fps[sp]->off_host[t], n = fps[sp]->off_host[t + 1] - o;
-      hdr[H.ds_pos + k] = put(s_wf[k], o, n, 0);
+      const int32_t o = P.wbeg[k][t], n = P.wbeg[k][t + 1] - o;
+      hdr[H.ds_pos + 2 * k] = n;
+      hdr[H.ds_pos + 2 * k + 1] = put(s_wf[k], o, n, 0);
     }
     {  // header section
       Section &S = secs[s_hdr];
@@ -2012,6 +2033,36 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         LT_CK_LAUNCH();
       }
       a += (int)L.desc.size();
+    }
+    // written rows per dataset as compact tile-local lists (store-back work items)
+    P.wlist.resize(ds_ptr.size());
+    P.wbeg.resize(ds_ptr.size());
+    for (size_t k = 0; k < ds_ptr.size(); ++k) {
+      if (!P.wflags[k].get()) continue;
+      const Footprint &fp = P.fp.at(ds_space[k]);
+      const int64_t n = fp.n;
+      DevBuf<int32_t> f32(std::max<int64_t>(n, 1), ctx.stream), scan(n + 1, ctx.stream);
+      int64_t cnt = 0;
+      if (n) {
+        k_u8_to_i32<<<grid_for(n, 256), 256, 0, ctx.stream>>>(P.wflags[k].get(), n, f32.get());
+        LT_CK_LAUNCH();
+        exclusive_sum(ctx, f32.get(), scan.get(), n);
+        cnt = last_plus(ctx, scan.get(), f32.get(), n);
+      }
+      k_set_int<<<1, 1, 0, ctx.stream>>>(scan.get() + n, (int32_t)cnt);
+      LT_CK_LAUNCH();
+      P.wlist[k].alloc(std::max<int64_t>(cnt, 1), ctx.stream);
+      if (n) {
+        k_compact_written<<<grid_for(n, 256), 256, 0, ctx.stream>>>(
+            P.wflags[k].get(), scan.get(), fp.tile.get(), fp.off.get(), n, P.wlist[k].get());
+        LT_CK_LAUNCH();
+      }
+      DevBuf<int32_t> wb(s->n_tiles + 1, ctx.stream);
+      k_gather_at<<<grid_for(s->n_tiles + 1, 256), 256, 0, ctx.stream>>>(scan.get(), fp.off.get(),
+                                                                         s->n_tiles + 1, wb.get());
+      LT_CK_LAUNCH();
+      to_host(ctx, wb, s->n_tiles + 1, P.wbeg[k]);
+      LT_CK(cudaStreamSynchronize(ctx.stream));
     }
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
     const size_t blob_max = build_blobs(ctx, s, cv, P, sp_index, ds_space);
