@@ -254,7 +254,8 @@ inline int dg_lanes(int k) {
   return dg_nd(k / 5 + 1);
 }
 // doubles of one per-side correction record: 5 NQ corrections, jf, face
-inline int dg_corr_size(int k) { return 5 * (k / 5 + 2) + 2; }
+// (record stride rounded up to odd: conflict-free 64-bit shared-memory reads)
+inline int dg_corr_size(int k) { return (5 * (k / 5 + 2) + 2) | 1; }
 inline bool dg_is_flux(int k) { return k % 5 == 1 || k % 5 == 2; }
 
 inline int64_t dg_param_count(int k) {

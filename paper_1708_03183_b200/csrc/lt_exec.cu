@@ -526,7 +526,9 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
         StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
         dispatch<FAM>(L.kernel, cx, lane);
       });
-      __syncthreads();
+      // the next loop runs the same (element, lane) items on the same threads
+      // and touches only this lane's components: no barrier needed
+      if (!L.nobar) __syncthreads();
       LT_TACC(8 + (j < 24 ? j : 23), t_loop);
       continue;
     }
@@ -1484,6 +1486,41 @@ static void build_runs(Ctx &ctx, const Footprint &fp, const uint8_t *flag, int n
   LT_CK(cudaStreamSynchronize(ctx.stream));
 }
 
+__global__ void k_differs(const int32_t *a, const int32_t *b, int64_t n, int32_t *flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && a[i] != b[i]) *flag = 1;
+}
+
+// Loops j and j+1 can share one pass of work items without a barrier: both
+// direct-only over the same space with identical tile lists, same lanes, and
+// kernels that touch only their lane's components (DG minv -> axpy).
+static bool barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &cv, int j) {
+  const LoopDesc &A = cv.loops[j], &Bq = cv.loops[j + 1];
+  auto lane_local = [](int k) {
+    return k >= K_DG_FIRST && ((k - K_DG_FIRST) % 5 == 3 || (k - K_DG_FIRST) % 5 == 4);
+  };
+  if (A.space != Bq.space || !lane_local(A.kernel) || !lane_local(Bq.kernel)) return false;
+  if (dg_lanes(A.kernel - K_DG_FIRST) != dg_lanes(Bq.kernel - K_DG_FIRST)) return false;
+  for (const lt_desc &d : A.desc)
+    if (d.map >= 0) return false;
+  for (const lt_desc &d : Bq.desc)
+    if (d.map >= 0) return false;
+  const LoopLists &La = s->lists[j], &Lb = s->lists[j + 1];
+  if (La.n != Lb.n) return false;
+  DevBuf<int32_t> flag(1, ctx.stream);
+  LT_CK(cudaMemsetAsync(flag.get(), 0, 4, ctx.stream));
+  k_differs<<<grid_for(s->n_tiles + 1, 256), 256, 0, ctx.stream>>>(
+      La.offsets.get(), Lb.offsets.get(), s->n_tiles + 1, flag.get());
+  if (La.n)
+    k_differs<<<grid_for(La.n, 256), 256, 0, ctx.stream>>>(La.elements.get(), Lb.elements.get(),
+                                                          La.n, flag.get());
+  LT_CK_LAUNCH();
+  int32_t f = 1;
+  LT_CK(cudaMemcpyAsync(&f, flag.get(), 4, cudaMemcpyDeviceToHost, ctx.stream));
+  LT_CK(cudaStreamSynchronize(ctx.stream));
+  return f == 0;
+}
+
 __global__ void k_u8_to_i32(const uint8_t *a, int64_t n, int32_t *b) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) b[i] = a[i];
@@ -2064,6 +2101,8 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       to_host(ctx, wb, s->n_tiles + 1, P.wbeg[k]);
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
+    for (int j = 0; j + 1 < nl; ++j)
+      P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, j) ? 1 : 0;
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
     const size_t blob_max = build_blobs(ctx, s, cv, P, sp_index, ds_space);
     H.blob = P.blob.get();
