@@ -426,6 +426,17 @@ __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, doub
   const int nrow = B[2 * S.sp];
   const int *idx = B + B[2 * S.sp + 1];
   const double *src = S.data;
+  if (S.vec) {  // 16-byte pairs: even rows, 16-byte aligned in HBM and shared memory
+    const int h = v >> 1;
+    int i = lt_div(threadIdx.x, h, S.magic), c = threadIdx.x - i * h;
+    while (i < nrow) {
+      cp_async16(rows + i * sv + 2 * c, src + ((uint32_t)idx[i] * (uint32_t)v + 2u * c));
+      i += S.di;
+      c += S.dc;
+      if (c >= h) { c -= h; ++i; }
+    }
+    return;
+  }
   int i = lt_div(threadIdx.x, v, S.magic), c = threadIdx.x - i * v;
   while (i < nrow) {
     cp_async8(rows + i * sv + c, src + ((uint32_t)idx[i] * (uint32_t)v + (uint32_t)c));
@@ -451,6 +462,7 @@ __device__ __forceinline__ void tile_prefetch(const StagedParams &P, int t, doub
   if (tid == 0) {
     int acc = P.blob_len[t] / 2;  // doubles after the blob (blob_len is a multiple of 4)
     for (int d = 0; d < P.n_ds; ++d) {
+      acc += acc & P.ds[d].vec;  // 16-byte aligned rows for pair copies
       base[d] = acc;
       acc += B[2 * P.ds[d].sp] * P.ds[d].stride;
     }
@@ -564,6 +576,19 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     const int *wl = B + B[P.ds_pos + 2 * d + 1];  // their footprint positions
     double *dst = S.data;
     const double *rows = smem + base[d];
+    if (S.vec) {
+      const int h = v >> 1;
+      int i = lt_div(tid, h, S.magic), c = tid - i * h;
+      while (i < nw) {
+        const int r = wl[i];
+        *reinterpret_cast<double2 *>(dst + ((uint32_t)idx[r] * (uint32_t)v + 2u * c)) =
+            *reinterpret_cast<const double2 *>(rows + r * sv + 2 * c);
+        i += S.di;
+        c += S.dc;
+        if (c >= h) { c -= h; ++i; }
+      }
+      continue;
+    }
     int i = lt_div(tid, v, S.magic), c = tid - i * v;
     while (i < nw) {
       const int r = wl[i];
@@ -1822,6 +1847,15 @@ static int exec_preference() {
   return 0;
 }
 
+// Shared-memory rows of a staged dataset: odd stride (conflict-free 64-bit
+// accesses) for odd vpe; for even vpe with 16-byte aligned data, 16-byte pair
+// copies need an even stride, kept = 2 (mod 4) so 64-bit accesses conflict at
+// most 2-way.
+static bool ds_vec(int v, const double *p) {
+  return v % 2 == 0 && reinterpret_cast<uintptr_t>(p) % 16 == 0;
+}
+static int ds_stride(int v, bool vec) { return vec ? (v % 4 == 2 ? v : v + 2) : (v | 1); }
+
 // Footprints, slot maps and written flags of the staged executor.  Returns
 // false (and leaves the plan untouched) when a footprint exceeds shared memory.
 static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_arg *args,
@@ -1878,7 +1912,7 @@ static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_
     size_t r = 0;
     for (size_t k = 0; k < ds_ptr.size(); ++k) {
       const auto &oh = P.fp[ds_space[k]].off_host;
-      r += (size_t)(oh[t + 1] - oh[t]) * (ds_vpe[k] | 1);
+      r += (size_t)(oh[t + 1] - oh[t]) * ds_stride(ds_vpe[k], ds_vec(ds_vpe[k], ds_ptr[k])) + 1;
     }
     regions_max = std::max(regions_max, r * sizeof(double));
   }
@@ -1968,7 +2002,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         LT_CK_LAUNCH();
         D.a[d].slot = LP.slots[d].get();
         D.a[d].ds = ds_of[a + d];
-        D.a[d].sstride = D.a[d].vpe | 1;
+        D.a[d].sstride = ds_stride(D.a[d].vpe, ds_vec(D.a[d].vpe, D.a[d].data));
       }
     }
     if (!LP.inc_desc.empty()) {
@@ -2038,10 +2072,12 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     for (size_t k = 0; k < ds_ptr.size(); ++k) {
       H.ds[k].data = ds_ptr[k];
       H.ds[k].vpe = ds_vpe[k];
-      H.ds[k].stride = ds_vpe[k] | 1;
-      H.ds[k].di = LT_SBLOCK / ds_vpe[k];
-      H.ds[k].dc = LT_SBLOCK % ds_vpe[k];
-      H.ds[k].magic = lt_magic(ds_vpe[k]);
+      H.ds[k].vec = ds_vec(ds_vpe[k], ds_ptr[k]) ? 1 : 0;
+      H.ds[k].stride = ds_stride(ds_vpe[k], H.ds[k].vec);
+      const int unit = H.ds[k].vec ? ds_vpe[k] / 2 : ds_vpe[k];  // pairs or doubles per row
+      H.ds[k].di = LT_SBLOCK / unit;
+      H.ds[k].dc = LT_SBLOCK % unit;
+      H.ds[k].magic = lt_magic(unit);
       H.ds[k].sp = sp_index.at(ds_space[k]);
       H.ds[k].load = 1;
       H.ds[k].ro = 1;

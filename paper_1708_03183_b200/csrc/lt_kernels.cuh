@@ -73,7 +73,8 @@ struct StageDS {
   // flattened (row, component) stepping over LT_SBLOCK threads, no runtime division
   int32_t di, dc;          // LT_SBLOCK / vpe, LT_SBLOCK % vpe
   uint32_t magic;          // x / vpe == umulhi(x, magic) for x < 2^16 (vpe >= 2)
-  int32_t pad;
+  int32_t vec;             // even vpe, 16-byte aligned: rows moved as 16-byte pairs
+                           // (di, dc, magic then count pairs, vpe / 2 per row)
 };
 
 // x / d for 0 <= x < 2^16, 1 <= d < 256, with magic = 2^32 / d + 1 (host: lt_magic)
