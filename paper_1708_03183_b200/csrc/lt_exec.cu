@@ -448,15 +448,19 @@ __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, doub
 
 // Phase 1 of a tile (no dependency on other tiles): tile program via TMA,
 // shared-memory layout, and the gather of datasets the chain never writes.
+__device__ __forceinline__ void tile_program_issue(const StagedParams &P, int t, double *smem,
+                                                   uint64_t *bar) {  // one thread
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of smem
+  bulk_load(smem, P.blob + P.blob_off[t], 4u * (unsigned)P.blob_len[t], bar);
+}
+
 __device__ __forceinline__ void tile_prefetch(const StagedParams &P, int t, double *smem,
-                                              int *base, uint64_t *bar, unsigned phase) {
+                                              int *base, uint64_t *bar, unsigned phase,
+                                              bool issued = false) {
   const int tid = threadIdx.x;
   int *B = reinterpret_cast<int *>(smem);
   LT_TSTAMP(t_blob);
-  if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of smem
-    bulk_load(B, P.blob + P.blob_off[t], 4u * (unsigned)P.blob_len[t], bar);
-  }
+  if (tid == 0 && !issued) tile_program_issue(P, t, smem, bar);
   mbar_wait(bar, phase);
   LT_TACC(0, t_blob);
   if (tid == 0) {
@@ -650,6 +654,15 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
   // a CTA still runs its items in queue order, so waits only target items
   // held by running CTAs and the schedule stays deadlock-free
   int next = threadIdx.x == 0 ? atomicAdd(D.queue, 1) : 0;
+  int prev = -1;  // tile whose completion is still to be released
+  // release: the barrier below orders every thread's store-back before thread
+  // 0's cumulative gpu-scope fence + increment (CUTLASS GenericBarrier's
+  // arrive); it is issued after the next tile program's TMA so the fence
+  // latency overlaps that load
+  auto release = [&](int tile) {
+    asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(D.done + tile)
+                 : "memory");
+  };
   for (;;) {
     if (threadIdx.x == 0) {
       item = next;
@@ -657,10 +670,17 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     }
     __syncthreads();
     const int it = item;
-    if (it >= D.n_items) return;
+    if (it >= D.n_items) {
+      if (threadIdx.x == 0 && prev >= 0) release(prev);
+      return;
+    }
     const int k = it / D.n_exec;
     const int t = D.order[it - k * D.n_exec];
-    tile_prefetch(P, t, smem, base, &bar, phase);  // overlaps the dependency wait
+    if (threadIdx.x == 0) {
+      tile_program_issue(P, t, smem, &bar);
+      if (prev >= 0) release(prev);
+    }
+    tile_prefetch(P, t, smem, base, &bar, phase, true);  // overlaps the dependency wait
     phase ^= 1u;
     const int n0 = D.nbr_off[t], n1 = D.nbr_off[t + 1];
     LT_TSTAMP(t_wait);
@@ -676,12 +696,7 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     LT_TACC(3, t_wait);
     LT_TSTAMP(t_tile);
     run_tile<FAM>(P, t, smem, base);
-    // release: barrier, then one cumulative gpu-scope fence + increment
-    // (the arrive pattern of CUTLASS's GenericBarrier)
-    __syncthreads();
-    if (threadIdx.x == 0)
-      asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(D.done + t)
-                   : "memory");
+    prev = t;
     LT_TACC(4, t_tile);
 #ifdef LT_PHASE_TIMING
     if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[5], 1ull);
