@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--chains", type=int, default=None,
+                    help="override chain executions per step (exploration only)")
     ap.add_argument("--untiled", action="store_true", help="time the untiled GPU executor")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the partitioned mesh")
@@ -300,6 +302,8 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.ts:
         cfg["ts"] = args.ts
+    if args.chains:
+        cfg["chains"] = args.chains
     import torch
     rank, world, local = (0, 1, 0)
     if args.impl == "reference":
