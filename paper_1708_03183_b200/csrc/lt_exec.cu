@@ -542,9 +542,9 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
         StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
         dispatch<FAM>(L.kernel, cx, lane);
       });
-      // the next loop runs the same (element, lane) items on the same threads
-      // and touches only this lane's components: no barrier needed
-      if (!L.nobar) __syncthreads();
+      // no barrier when the next loop's first phase cannot conflict with this
+      // one (plan: barrier_free_pair); an empty next loop needs the barrier
+      if (!L.nobar || (j + 1 < P.n_loops && B[P.loop_pos[j + 1]] == 0)) __syncthreads();
       LT_TACC(8 + (j < 24 ? j : 23), t_loop);
       continue;
     }
@@ -1531,11 +1531,36 @@ __global__ void k_differs(const int32_t *a, const int32_t *b, int64_t n, int32_t
   if (i < n && a[i] != b[i]) *flag = 1;
 }
 
-// Loops j and j+1 can share one pass of work items without a barrier: both
-// direct-only over the same space with identical tile lists, same lanes, and
-// kernels that touch only their lane's components (DG minv -> axpy).
-static bool barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &cv, int j) {
+// No barrier is needed between a direct loop j (no INC) and the first phase of
+// loop j+1 when either
+//  (a) both are direct-only over the same space with identical tile lists and
+//      the same lanes, and their kernels touch only their lane's components
+//      (DG inverse mass -> axpy): every thread re-runs its own items; or
+//  (b) loop j+1's first phase (its body; INC bodies write only scratch) neither
+//      reads nor writes a dataset loop j writes, and writes nothing loop j
+//      reads (DG volume -> interior-facet records).
+static bool barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &cv,
+                              const lt_arg *args, int j) {
   const LoopDesc &A = cv.loops[j], &Bq = cv.loops[j + 1];
+  for (const lt_desc &d : A.desc)
+    if (d.map >= 0 && d.mode != LT_READ) return false;  // loop j must not have an apply phase
+  int a0 = 0;
+  for (int q = 0; q < j; ++q) a0 += (int)cv.loops[q].desc.size();
+  const lt_arg *aa = args + a0, *ab = aa + A.desc.size();
+  // (b) dataset independence
+  bool indep = true;
+  for (size_t x = 0; x < A.desc.size() && indep; ++x) {
+    const bool a_writes = A.desc[x].mode != LT_READ;
+    for (size_t y = 0; y < Bq.desc.size() && indep; ++y) {
+      if (aa[x].values != ab[y].values) continue;
+      const bool b_body_writes = Bq.desc[y].map < 0 && Bq.desc[y].mode != LT_READ;
+      const bool b_body_reads = Bq.desc[y].mode == LT_READ || Bq.desc[y].mode == LT_RW;
+      if (a_writes && (b_body_reads || b_body_writes)) indep = false;
+      if (!a_writes && b_body_writes) indep = false;
+    }
+  }
+  if (indep) return true;
+  // (a) same items, lane-local kernels
   auto lane_local = [](int k) {
     return k >= K_DG_FIRST && ((k - K_DG_FIRST) % 5 == 3 || (k - K_DG_FIRST) % 5 == 4);
   };
@@ -2153,7 +2178,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
     for (int j = 0; j + 1 < nl; ++j)
-      P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, j) ? 1 : 0;
+      P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j) ? 1 : 0;
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
     const size_t blob_max = build_blobs(ctx, s, cv, P, sp_index, ds_space);
     H.blob = P.blob.get();
