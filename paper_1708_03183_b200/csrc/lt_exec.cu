@@ -1249,7 +1249,7 @@ static const size_t kSmemBudget = 96 * 1024;
 // (smaller chunks: more apply phases, more resident tiles per SM)
 static size_t scratch_budget() {
   const char *e = getenv("LT_SCRATCH_KB");
-  return (e ? (size_t)atoi(e) : 24) * 1024;
+  return (e ? (size_t)atoi(e) : 8) * 1024;
 }
 static std::string g_last_fit;
 static const size_t kSmemMax = 227 * 1024;
