@@ -526,10 +526,24 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       const int CH = L.chunk;
       const int *pb = LH + 2 + L.n_desc;
       for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
-        for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
-          StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
-          dispatch<FAM>(L.kernel, cx, lane);
-        });
+        if (FAM >= 1 && FAM <= 4) {  // kernel selected once per loop, not per item
+          constexpr int PP = FAM >= 1 && FAM <= 4 ? FAM : 1;
+          if ((L.kernel - K_DG_FIRST) % 5 == 1)
+            for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
+              StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+              dg_iflux<PP>(cx, lane);
+            });
+          else
+            for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
+              StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+              dg_eflux<PP>(cx, lane);
+            });
+        } else {
+          for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
+            StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+            dispatch<FAM>(L.kernel, cx, lane);
+          });
+        }
         __syncthreads();
         apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base);
         __syncthreads();
@@ -538,10 +552,30 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       continue;
     }
     if (!L.n_inc) {  // direct / mapped-read loop: all items of the list at once
-      for_items_s(n, L, [&](int pos, int lane) {
-        StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
-        dispatch<FAM>(L.kernel, cx, lane);
-      });
+      const int which = (L.kernel - K_DG_FIRST) % 5;
+      if (FAM >= 1 && FAM <= 4 && L.kernel >= K_DG_FIRST) {  // kernel selected once per loop
+        constexpr int PP = FAM >= 1 && FAM <= 4 ? FAM : 1;
+        if (which == 0)
+          for_items_s(n, L, [&](int pos, int lane) {
+            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            dg_vol<PP>(cx, lane);
+          });
+        else if (which == 3)
+          for_items_s(n, L, [&](int pos, int lane) {
+            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            dg_minv<PP>(cx, lane);
+          });
+        else
+          for_items_s(n, L, [&](int pos, int lane) {
+            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            dg_axpy<PP>(cx, lane);
+          });
+      } else {
+        for_items_s(n, L, [&](int pos, int lane) {
+          StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+          dispatch<FAM>(L.kernel, cx, lane);
+        });
+      }
       // no barrier when the next loop's first phase cannot conflict with this
       // one (plan: barrier_free_pair); an empty next loop needs the barrier
       if (!L.nobar || (j + 1 < P.n_loops && B[P.loop_pos[j + 1]] == 0)) __syncthreads();
