@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <tuple>
@@ -298,7 +299,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 #ifdef LT_PHASE_TIMING
 // profiling build only: per-phase cycle totals of the staged executor (thread 0)
-__device__ unsigned long long g_phase_cycles[40];
+__device__ unsigned long long g_phase_cycles[64];
 #define LT_TSTAMP(var) long long var = clock64()
 #define LT_TACC(slot, t0)                                                  \
   do {                                                                     \
@@ -418,32 +419,71 @@ __device__ __forceinline__ void apply_plan(const DLoop &L, int p, const int *gc_
   }
 }
 
-// Gather the (row, component)-flattened footprint rows of dataset d into its
-// odd-stride shared rows with asynchronous 8-byte copies (coalesced within rows
-// and along runs of consecutive ids).
+// Gather the footprint rows of dataset d into its shared rows with
+// asynchronous copies.  Each thread owns one component (or 16-byte pair) c and
+// a row offset r0 < S.di = LT_SBLOCK / unit, and walks rows r0, r0 + di, ...:
+// consecutive threads copy consecutive components of a row (coalesced within
+// rows and along runs of consecutive ids), and the loop carries no division
+// or component wrap-around (4-5 instructions per copy).
 __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, double *rows) {
-  const int v = S.vpe, sv = S.stride;
+  const uint32_t v = (uint32_t)S.vpe;
+  const int rpp = S.di;
   const int nrow = B[2 * S.sp];
   const int *idx = B + B[2 * S.sp + 1];
+  const int unit = S.vec ? (int)v >> 1 : (int)v;
+  const int r0 = lt_div(threadIdx.x, unit, S.magic);
+  if (r0 >= rpp) return;
+  const uint32_t c = (uint32_t)(threadIdx.x - r0 * unit) << S.vec;  // thread's first double
   const double *src = S.data;
+  double *dst = rows + r0 * S.stride + c;
+  const int step = rpp * S.stride;
   if (S.vec) {  // 16-byte pairs: even rows, 16-byte aligned in HBM and shared memory
-    const int h = v >> 1;
-    int i = lt_div(threadIdx.x, h, S.magic), c = threadIdx.x - i * h;
-    while (i < nrow) {
-      cp_async16(rows + i * sv + 2 * c, src + ((uint32_t)idx[i] * (uint32_t)v + 2u * c));
-      i += S.di;
-      c += S.dc;
-      if (c >= h) { c -= h; ++i; }
-    }
+    for (int i = r0; i < nrow; i += rpp, dst += step) cp_async16(dst, src + ((uint32_t)idx[i] * v + c));
     return;
   }
-  int i = lt_div(threadIdx.x, v, S.magic), c = threadIdx.x - i * v;
-  while (i < nrow) {
-    cp_async8(rows + i * sv + c, src + ((uint32_t)idx[i] * (uint32_t)v + (uint32_t)c));
-    i += S.di;
-    c += S.dc;
-    if (c >= v) { c -= v; ++i; }
+  for (int i = r0; i < nrow; i += rpp, dst += step) cp_async8(dst, src + ((uint32_t)idx[i] * v + c));
+}
+
+// Store back the rows of dataset S the tile wrote (compact list wl of
+// footprint positions), same thread mapping as the gather.  Rows go in batches
+// of SB: all shared-memory loads of a batch are issued before its
+// global stores (the stores may alias nothing the loads read, but the compiler
+// cannot know), so the wl -> idx -> row load chains overlap.
+template <int SB, class T>
+__device__ __forceinline__ void store_rows_t(double *dst, const double *src, const int *idx,
+                                            const int *wl, int nw, int r0, int rpp, uint32_t v,
+                                            int sv) {
+  for (int i = r0; i < nw; i += SB * rpp) {
+    int r[SB];
+    uint32_t g[SB];
+    T x[SB];
+#pragma unroll
+    for (int k = 0; k < SB; ++k) r[k] = i + k * rpp < nw ? wl[i + k * rpp] : -1;
+#pragma unroll
+    for (int k = 0; k < SB; ++k)
+      if (r[k] >= 0) {
+        g[k] = (uint32_t)idx[r[k]] * v;
+        x[k] = *reinterpret_cast<const T *>(src + r[k] * sv);
+      }
+#pragma unroll
+    for (int k = 0; k < SB; ++k)
+      if (r[k] >= 0) *reinterpret_cast<T *>(dst + g[k]) = x[k];
   }
+}
+
+template <int SB>
+__device__ __forceinline__ void store_rows(const StageDS &S, const int *idx, const int *wl, int nw,
+                                          const double *rows) {
+  const uint32_t v = (uint32_t)S.vpe;
+  const int rpp = S.di;
+  const int unit = S.vec ? (int)v >> 1 : (int)v;
+  const int r0 = lt_div(threadIdx.x, unit, S.magic);
+  if (r0 >= rpp) return;
+  const uint32_t c = (uint32_t)(threadIdx.x - r0 * unit) << S.vec;
+  if (S.vec)
+    store_rows_t<SB, double2>(S.data + c, rows + c, idx, wl, nw, r0, rpp, v, S.stride);
+  else
+    store_rows_t<SB, double>(S.data + c, rows + c, idx, wl, nw, r0, rpp, v, S.stride);
 }
 
 // Phase 1 of a tile (no dependency on other tiles): tile program via TMA,
@@ -505,7 +545,7 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
 
 // Phase 2: gather the datasets the chain writes, run every loop on shared
 // memory, store back the rows this tile wrote.
-template <int FAM>
+template <int FAM, int SB = 1>
 __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base) {
   const int tid = threadIdx.x;
   const int *B = reinterpret_cast<const int *>(smem);
@@ -526,6 +566,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       const int CH = L.chunk;
       const int *pb = LH + 2 + L.n_desc;
       for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
+        LT_TSTAMP(t_rec);
         if (FAM >= 1 && FAM <= 4) {  // kernel selected once per loop, not per item
           constexpr int PP = FAM >= 1 && FAM <= 4 ? FAM : 1;
           if ((L.kernel - K_DG_FIRST) % 5 == 1)
@@ -545,6 +586,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
           });
         }
         __syncthreads();
+        LT_TACC(40 + (j < 23 ? j : 23), t_rec);
         apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base);
         __syncthreads();
       }
@@ -603,38 +645,12 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     LT_TACC(8 + (j < 24 ? j : 23), t_loop);
   }
   LT_TSTAMP(t_wb);
-  // store back the rows this tile wrote (flattened like the gather, coalesced)
+  // store back the rows this tile wrote (coalesced like the gather)
   for (int d = 0; d < P.n_ds; ++d) {
     const StageDS &S = P.ds[d];
     if (!S.written) continue;
-    const int v = S.vpe, sv = S.stride;
-    const int nrow = B[2 * S.sp];
-    const int *idx = B + B[2 * S.sp + 1];
-    const int nw = B[P.ds_pos + 2 * d];          // rows this tile wrote
-    const int *wl = B + B[P.ds_pos + 2 * d + 1];  // their footprint positions
-    double *dst = S.data;
-    const double *rows = smem + base[d];
-    if (S.vec) {
-      const int h = v >> 1;
-      int i = lt_div(tid, h, S.magic), c = tid - i * h;
-      while (i < nw) {
-        const int r = wl[i];
-        *reinterpret_cast<double2 *>(dst + ((uint32_t)idx[r] * (uint32_t)v + 2u * c)) =
-            *reinterpret_cast<const double2 *>(rows + r * sv + 2 * c);
-        i += S.di;
-        c += S.dc;
-        if (c >= h) { c -= h; ++i; }
-      }
-      continue;
-    }
-    int i = lt_div(tid, v, S.magic), c = tid - i * v;
-    while (i < nw) {
-      const int r = wl[i];
-      dst[(uint32_t)idx[r] * (uint32_t)v + (uint32_t)c] = rows[r * sv + c];
-      i += S.di;
-      c += S.dc;
-      if (c >= v) { c -= v; ++i; }
-    }
+    store_rows<SB>(S, B + B[2 * S.sp + 1], B + B[P.ds_pos + 2 * d + 1], B[P.ds_pos + 2 * d],
+               smem + base[d]);
   }
   LT_TACC(2, t_wb);
 }
@@ -675,8 +691,12 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
   return v;
 }
 
-template <int FAM>
-__global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ StagedParams P,
+// MINB: CTAs per SM the register budget is sized for (7: 72 registers, the
+// occupancy small tile programs reach; 4: 128 registers for footprints whose
+// shared memory allows at most 4 CTAs per SM -- those tiles are long enough
+// that batched store-back and unspilled bodies pay)
+template <int FAM, int MINB>
+__global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_constant__ StagedParams P,
                                                         const DataflowArgs D) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int base[LT_MAX_STAGED + 1];
@@ -729,7 +749,7 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_dataflow(const __grid_constant__ 
     __syncthreads();
     LT_TACC(3, t_wait);
     LT_TSTAMP(t_tile);
-    run_tile<FAM>(P, t, smem, base);
+    run_tile<FAM, (MINB >= 7 ? 1 : 4)>(P, t, smem, base);
     prev = t;
     LT_TACC(4, t_tile);
 #ifdef LT_PHASE_TIMING
@@ -1079,10 +1099,13 @@ struct ExecPlan {
   DevBuf<int32_t> blob, blob_len;
   DevBuf<int64_t> blob_off;
   size_t data_max = 0;  // largest per-tile dataset rows (bytes)
+  std::vector<size_t> tile_rows;   // per tile: dataset-row bytes (diagnostics)
+  std::vector<int32_t> tile_blob;  // per tile: tile-program ints (diagnostics)
   // dataflow
   bool dataflow = false;
   DevBuf<int32_t> order_all, order_core, order_bnd, nbr_off, nbr, done, queue;
   int n_all = 0, n_core = 0, n_bnd = 0, grid = 0;
+  bool wide = false;  // 128-register build (tile programs allow <= 4 CTAs per SM)
 };
 
 static int choose_chunk(int scratch_per_pos, size_t smem_budget, int block) {
@@ -1804,6 +1827,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   }
   (void)n_exec;
   (void)ds_space;
+  P.tile_blob = blen;
   return blob_max;
 }
 
@@ -1981,6 +2005,7 @@ static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_
   for (auto &kv : sources) build_footprint(ctx, s, cv, kv.second, P.region, P.fp[kv.first]);
   // shared-memory regions of the largest tile: footprint ids + dataset rows
   regions_max = 0;
+  P.tile_rows.assign(s->n_tiles, 0);
   for (int t = 0; t < s->n_tiles; ++t) {
     if (s->region[t] == LT_NONEXEC) continue;
     size_t r = 0;
@@ -1989,9 +2014,38 @@ static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_
       r += (size_t)(oh[t + 1] - oh[t]) * ds_stride(ds_vpe[k], ds_vec(ds_vpe[k], ds_ptr[k])) + 1;
     }
     regions_max = std::max(regions_max, r * sizeof(double));
+    P.tile_rows[t] = r * sizeof(double);
   }
   P.data_max = regions_max;
   return regions_max + 16 * 1024 <= kSmemMax;
+}
+
+// LT_DEBUG_PLAN=1: shared-memory composition and per-tile size percentiles
+static void print_plan_stats(const lt_schedule *s, const ExecPlan &P, size_t blob_max,
+                             size_t scratch_max) {
+  std::vector<size_t> rows, blob, tot;
+  for (int t = 0; t < s->n_tiles; ++t) {
+    if (s->region[t] == LT_NONEXEC) continue;
+    rows.push_back(P.tile_rows[t]);
+    blob.push_back(4 * (size_t)P.tile_blob[t]);
+    tot.push_back(P.tile_rows[t] + 4 * (size_t)P.tile_blob[t]);
+  }
+  auto pct = [](std::vector<size_t> v, double q) -> size_t {
+    if (v.empty()) return 0;
+    std::sort(v.begin(), v.end());
+    return v[std::min(v.size() - 1, (size_t)(q * (double)v.size()))];
+  };
+  fprintf(stderr, "[lt plan] tiles %zu smem %zu = blob_max %zu + rows_max %zu + scratch %zu\n",
+          rows.size(), P.smem_bytes, blob_max, P.data_max, scratch_max);
+  const char *nm[3] = {"rows", "blob", "rows+blob"};
+  const std::vector<size_t> *vv[3] = {&rows, &blob, &tot};
+  for (int i = 0; i < 3; ++i)
+    fprintf(stderr, "[lt plan]   %-9s p50 %zu p90 %zu p99 %zu max %zu\n", nm[i], pct(*vv[i], 0.5),
+            pct(*vv[i], 0.9), pct(*vv[i], 0.99), pct(*vv[i], 1.0));
+  for (int j = 0; j < s->n_loops; ++j)
+    fprintf(stderr, "[lt plan]   loop %d chunk %d scratch/pos %d deferred %d nobar %d\n", j,
+            P.loops[j].chunk, P.loops[j].scratch_per_pos, (int)P.loops[j].deferred,
+            (int)P.host_loops[j].nobar);
 }
 
 static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const ChainView &cv,
@@ -2225,6 +2279,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       return nullptr;
     }
     P.smem_bytes = blob_max + P.data_max + scratch_max;
+    if (getenv("LT_DEBUG_PLAN")) print_plan_stats(s, P, blob_max, scratch_max);
     if (P.dataflow) build_dependencies(ctx, s, P);
   } else {
     P.smem_bytes = scratch_max;
@@ -2263,14 +2318,21 @@ static StagedFn staged_fn(int fam) {
 }
 
 typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
-static DataflowFn dataflow_fn(int fam) {
+static DataflowFn dataflow_fn(int fam, bool wide = false) {
+  if (wide) switch (fam) {
+      case 1: return k_dataflow<1, 4>;
+      case 2: return k_dataflow<2, 4>;
+      case 3: return k_dataflow<3, 4>;
+      case 4: return k_dataflow<4, 4>;
+      default: break;
+    }
   switch (fam) {
-    case 0: return k_dataflow<0>;
-    case 1: return k_dataflow<1>;
-    case 2: return k_dataflow<2>;
-    case 3: return k_dataflow<3>;
-    case 4: return k_dataflow<4>;
-    default: return k_dataflow<5>;
+    case 0: return k_dataflow<0, 7>;
+    case 1: return k_dataflow<1, 7>;
+    case 2: return k_dataflow<2, 7>;
+    case 3: return k_dataflow<3, 7>;
+    case 4: return k_dataflow<4, 7>;
+    default: return k_dataflow<5, 7>;
   }
 }
 
@@ -2297,7 +2359,31 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   }
   ExecPlan &P = *s->plan;
   const int fam = chain_family(cv);
-  const void *fn = P.dataflow  ? (const void *)dataflow_fn(fam)
+  if (P.dataflow && P.grid == 0) {
+    // register budget: the 72-register build reaches 7 CTAs per SM; when the
+    // tile programs' shared memory allows at most 4, the 128-register build
+    // costs no occupancy and spills nothing
+    int per_sm = 0, sms = 0;
+    const void *narrow = (const void *)dataflow_fn(fam, false);
+    if (P.smem_bytes > 48 * 1024)
+      LT_CK(cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)P.smem_bytes));
+    LT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, narrow, LT_SBLOCK, P.smem_bytes));
+    P.wide = per_sm <= 4 && fam >= 1 && fam <= 4 && !getenv("LT_NARROW");
+    if (P.wide) {
+      const void *w = (const void *)dataflow_fn(fam, true);
+      if (P.smem_bytes > 48 * 1024)
+        LT_CK(cudaFuncSetAttribute(w, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)P.smem_bytes));
+      LT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, w, LT_SBLOCK, P.smem_bytes));
+    }
+    LT_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
+    P.grid = std::max(1, per_sm) * sms;
+    if (getenv("LT_DEBUG_PLAN"))
+      fprintf(stderr, "[lt plan] dataflow %s build, %d CTAs/SM, grid %d\n",
+              P.wide ? "128-register" : "72-register", per_sm, P.grid);
+  }
+  const void *fn = P.dataflow  ? (const void *)dataflow_fn(fam, P.wide)
                    : P.staged ? (const void *)staged_fn(fam)
                               : (const void *)fused_fn(fam);
   if (P.smem_bytes > 48 * 1024)
@@ -2306,12 +2392,6 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   int launches = 0, colors = 0;
   int64_t visits = 0;
   if (P.dataflow) {
-    if (P.grid == 0) {
-      int per_sm = 0, sms = 0;
-      LT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LT_SBLOCK, P.smem_bytes));
-      LT_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device));
-      P.grid = std::max(1, per_sm) * sms;
-    }
     const bool core = phases & LT_PHASE_CORE, bnd = phases & LT_PHASE_BOUNDARY;
     DataflowArgs D;
     D.order = core && bnd ? P.order_all.get() : core ? P.order_core.get() : P.order_bnd.get();
@@ -2325,7 +2405,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       LT_CK(cudaMemsetAsync(P.done.get(), 0, 4 * P.done.n, ctx.stream));
     LT_CK(cudaMemsetAsync(P.queue.get(), 0, 4, ctx.stream));
     if (D.n_items > 0) {
-      dataflow_fn(fam)<<<std::min(P.grid, D.n_items), LT_SBLOCK, P.smem_bytes, ctx.stream>>>(P.sp,
+      dataflow_fn(fam, P.wide)<<<std::min(P.grid, D.n_items), LT_SBLOCK, P.smem_bytes, ctx.stream>>>(P.sp,
                                                                                          D);
       LT_CK_LAUNCH();
       ++launches;
@@ -2493,9 +2573,9 @@ extern "C" int lt_kernel_count(void) { return kNumKernels; }
 
 #ifdef LT_PHASE_TIMING
 extern "C" int lt_phase_cycles(unsigned long long *out, int reset) {
-  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 40);
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 64);
   if (reset) {
-    static unsigned long long zero[40] = {0};
+    static unsigned long long zero[64] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, zero, sizeof(zero));
   }
   return 0;

@@ -70,8 +70,8 @@ struct StageDS {
   int32_t load;            // 0: every footprint row is written before it is read
   int32_t written;         // the tile writes some rows of it (store-back flags present)
   int32_t ro;              // never written by the chain: gathered before dependency waits
-  // flattened (row, component) stepping over LT_SBLOCK threads, no runtime division
-  int32_t di, dc;          // LT_SBLOCK / vpe, LT_SBLOCK % vpe
+  // gather/store-back thread mapping: thread = (row offset < di, component < unit)
+  int32_t di, dc;          // rows per pass LT_SBLOCK / unit, LT_SBLOCK % unit (unit: vpe or pairs)
   uint32_t magic;          // x / vpe == umulhi(x, magic) for x < 2^16 (vpe >= 2)
   int32_t vec;             // even vpe, 16-byte aligned: rows moved as 16-byte pairs
                            // (di, dc, magic then count pairs, vpe / 2 per row)
