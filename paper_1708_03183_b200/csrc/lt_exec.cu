@@ -327,6 +327,8 @@ struct StagedParams {
   int32_t n_loops, n_ds, n_sp, hs;   // hs: header ints
   int32_t loop_pos[LT_MAX_SLOOPS];   // header position of each loop's block
   int32_t ds_pos;                    // header position of the written-row lists
+  int32_t prog_pos;                  // header position of the program length (ints)
+  int32_t ro_packed;                 // rows of read-only datasets follow the program in the blob
   int32_t pad;
   const int32_t *blob;
   const int64_t *blob_off;           // per tile: first int of its blob
@@ -504,18 +506,24 @@ __device__ __forceinline__ void tile_prefetch(const StagedParams &P, int t, doub
   mbar_wait(bar, phase);
   LT_TACC(0, t_blob);
   if (tid == 0) {
-    int acc = P.blob_len[t] / 2;  // doubles after the blob (blob_len is a multiple of 4)
-    for (int d = 0; d < P.n_ds; ++d) {
-      acc += acc & P.ds[d].vec;  // 16-byte aligned rows for pair copies
-      base[d] = acc;
-      acc += B[2 * P.ds[d].sp] * P.ds[d].stride;
-    }
+    // rows after the program (a multiple of 4 ints): read-only datasets first
+    // (with ro_packed the blob already holds them there), then the others
+    int acc = B[P.prog_pos] / 2;
+    for (int pass = 1; pass >= 0; --pass)
+      for (int d = 0; d < P.n_ds; ++d) {
+        if (P.ds[d].ro != pass) continue;
+        acc += acc & P.ds[d].vec;  // 16-byte aligned rows for pair copies
+        base[d] = acc;
+        acc += B[2 * P.ds[d].sp] * P.ds[d].stride;
+      }
     base[P.n_ds] = acc;
   }
   __syncthreads();
-  for (int d = 0; d < P.n_ds; ++d)
-    if (P.ds[d].ro) gather_rows(P.ds[d], B, smem + base[d]);
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (!P.ro_packed) {
+    for (int d = 0; d < P.n_ds; ++d)
+      if (P.ds[d].ro) gather_rows(P.ds[d], B, smem + base[d]);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
 }
 
 // Deferred apply of a DG facet loop's chunk: one work item per (unique target,
@@ -666,6 +674,33 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_staged_tiles(const __grid_constan
   __syncthreads();
   tile_prefetch(P, tile_ids[blockIdx.x], smem, base, &bar, 0);
   run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base);
+}
+
+// Pack the rows of the read-only datasets of every tile to be run behind its
+// tile program, in the shared-memory layout tile_prefetch computes, so that
+// the tile's single bulk copy brings them along.  Runs once per execution call
+// (datasets may change between calls; they cannot change within one).
+__global__ void __launch_bounds__(256) k_pack_ro(const __grid_constant__ StagedParams P,
+                                                 const int32_t *__restrict__ order, int n) {
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    const int t = order[it];
+    const int32_t *B = P.blob + P.blob_off[t];
+    double *tile = reinterpret_cast<double *>(const_cast<int32_t *>(B));
+    int acc = B[P.prog_pos] / 2;
+    for (int d = 0; d < P.n_ds; ++d) {
+      const StageDS &S = P.ds[d];
+      if (!S.ro) continue;
+      acc += acc & S.vec;
+      const int v = S.vpe, nrow = B[2 * S.sp];
+      const int32_t *idx = B + B[2 * S.sp + 1];
+      double *rows = tile + acc;
+      for (int w = threadIdx.x; w < nrow * v; w += blockDim.x) {
+        const int r = w / v, c = w - r * v;
+        rows[r * S.stride + c] = __ldg(S.data + ((uint32_t)idx[r] * (uint32_t)v + c));
+      }
+      acc += nrow * S.stride;
+    }
+  }
 }
 
 // Persistent dataflow executor: CTAs pop tile instances (repeat k, tile) from a
@@ -1097,6 +1132,7 @@ struct ExecPlan {
   std::vector<int32_t> rank;  // execution order key: colour refined by write-conflict sub-colour
   int max_subcolor = 0;
   DevBuf<int32_t> blob, blob_len;
+  DevBuf<int32_t> blob_len_full;  // program + packed read-only rows (ints), when packable
   DevBuf<int64_t> blob_off;
   size_t data_max = 0;  // largest per-tile dataset rows (bytes)
   std::vector<size_t> tile_rows;   // per tile: dataset-row bytes (diagnostics)
@@ -1672,6 +1708,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   }
   H.ds_pos = hp;
   hp += 2 * H.n_ds;
+  H.prog_pos = hp++;
   H.hs = hp;
   // host copies of the per-tile ranges
   std::vector<std::vector<int32_t>> off(nl), cb(nl);
@@ -1699,7 +1736,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
     return secs.back();
   };
   std::vector<int32_t> hdr_host;
-  std::vector<int32_t> blen(nt, 0);
+  std::vector<int32_t> blen(nt, 0), bfull(nt, 0);
   std::vector<int64_t> boff(nt, 0);
   size_t blob_max = 0;
   int64_t total = 0;
@@ -1782,6 +1819,8 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       hdr[H.ds_pos + 2 * k] = n;
       hdr[H.ds_pos + 2 * k + 1] = put(s_wf[k], o, n, 0);
     }
+    cur = (cur + 3) / 4 * 4;  // 16-byte aligned programs
+    hdr[H.prog_pos] = (int32_t)cur;
     {  // header section
       Section &S = secs[s_hdr];
       S.src_off.push_back((int64_t)hdr_host.size());
@@ -1790,17 +1829,32 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       S.sub.push_back(0);
       hdr_host.insert(hdr_host.end(), hdr.begin(), hdr.end());
     }
-    cur = (cur + 3) / 4 * 4;  // 16-byte aligned blobs
+    blob_max = std::max(blob_max, (size_t)cur * 4);
     blen[t] = (int32_t)cur;
+    if (H.ro_packed) {  // room for the read-only rows behind the program (k_pack_ro)
+      int64_t acc = cur / 2;
+      for (int k = 0; k < H.n_ds; ++k) {
+        if (!H.ds[k].ro) continue;
+        acc += acc & H.ds[k].vec;
+        const auto &oh = fps[H.ds[k].sp]->off_host;
+        acc += (int64_t)(oh[t + 1] - oh[t]) * H.ds[k].stride;
+      }
+      cur = (2 * acc + 3) / 4 * 4;
+    }
+    bfull[t] = (int32_t)cur;
     boff[t] = total;
     total += cur;
-    blob_max = std::max(blob_max, (size_t)cur * 4);
   }
   P.blob.alloc(std::max<int64_t>(total, 4), ctx.stream);
   P.blob_off.alloc(nt, ctx.stream);
   P.blob_len.alloc(nt, ctx.stream);
   LT_CK(cudaMemcpyAsync(P.blob_off.get(), boff.data(), 8 * nt, cudaMemcpyHostToDevice, ctx.stream));
   LT_CK(cudaMemcpyAsync(P.blob_len.get(), blen.data(), 4 * nt, cudaMemcpyHostToDevice, ctx.stream));
+  if (H.ro_packed) {
+    P.blob_len_full.alloc(nt, ctx.stream);
+    LT_CK(cudaMemcpyAsync(P.blob_len_full.get(), bfull.data(), 4 * nt, cudaMemcpyHostToDevice,
+                          ctx.stream));
+  }
   DevBuf<int32_t> hdr_dev(std::max<int64_t>((int64_t)hdr_host.size(), 1), ctx.stream);
   if (!hdr_host.empty())
     LT_CK(cudaMemcpyAsync(hdr_dev.get(), hdr_host.data(), 4 * hdr_host.size(),
@@ -2213,6 +2267,13 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     for (int j = 0, q = 0; j < nl; ++j)
       for (size_t d = 0; d < cv.loops[j].desc.size(); ++d, ++q)
         if (cv.loops[j].desc[d].mode != LT_READ) H.ds[ds_of[q]].ro = 0;
+    // dataflow: blobs leave room for the read-only rows of every tile behind
+    // its program; repeated executions pack them there (k_pack_ro, once per
+    // call) so they arrive with the program in one bulk copy.  H.ro_packed
+    // marks the plan packable; each launch sets it for its own parameters.
+    H.ro_packed = 0;
+    if (P.dataflow)
+      for (int k = 0; k < H.n_ds; ++k) H.ro_packed |= H.ds[k].ro;
     a = 0;
     for (int j = 0; j < nl; ++j) {
       const LoopDesc &L = cv.loops[j];
@@ -2404,9 +2465,19 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     if (core)  // a boundary-only call continues the counters of its core call
       LT_CK(cudaMemsetAsync(P.done.get(), 0, 4 * P.done.n, ctx.stream));
     LT_CK(cudaMemsetAsync(P.queue.get(), 0, 4, ctx.stream));
+    // packing costs one pass over the read-only rows: it pays when every tile
+    // runs more than once in this call
+    StagedParams sp = P.sp;
+    sp.ro_packed = P.sp.ro_packed && repeats >= 2 && !getenv("LT_NO_PACK");
+    if (sp.ro_packed) sp.blob_len = P.blob_len_full.get();
+    if (D.n_items > 0 && sp.ro_packed) {
+      k_pack_ro<<<std::min(D.n_exec, 16 * 148), 256, 0, ctx.stream>>>(sp, D.order, D.n_exec);
+      LT_CK_LAUNCH();
+      ++launches;
+    }
     if (D.n_items > 0) {
-      dataflow_fn(fam, P.wide)<<<std::min(P.grid, D.n_items), LT_SBLOCK, P.smem_bytes, ctx.stream>>>(P.sp,
-                                                                                         D);
+      dataflow_fn(fam, P.wide)<<<std::min(P.grid, D.n_items), LT_SBLOCK, P.smem_bytes, ctx.stream>>>(
+          sp, D);
       LT_CK_LAUNCH();
       ++launches;
     }

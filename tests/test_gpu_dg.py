@@ -86,3 +86,28 @@ def test_gpu_dg_repeat_equals_sequential_calls(repeats):
     TiledRunner(s2, b.chain, b.bindings, b.datasets, b.registry, repeats=repeats)
     for n in ("u", "s", "ru", "rs"):
         np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
+
+
+@pytest.mark.parametrize("p,steps", [(1, 1), (2, 2)])
+def test_gpu_dg_repeat_repacks_constants_each_call(p, steps):
+    """Repeated execution packs the read-only rows (geometry, material) into the
+    tile programs once per call: a change of a read-only dataset between calls
+    must be seen by the next call."""
+    from paper_1708_03183_b200.dg import elastic_setup
+    from paper_1708_03183_b200.executor import TiledRunner
+    mk = lambda: elastic_problem(elastic_setup(36, 28, p, steps, material=("uniform", 5),
+                                               sigma=5.0))
+    a, b = mk(), mk()
+    a.install_params()
+    sa = lt.inspect_chain(a.chain, 24, lt.ExecMode.SHARED)
+    sb = lt.inspect_chain(b.chain, 24, lt.ExecMode.SHARED)
+    runner = TiledRunner(sb, b.chain, b.bindings, b.datasets, b.registry, repeats=2)
+    for _ in range(2):
+        lt.execute_schedule(sa, a.chain, a.bindings, a.datasets, a.registry, use_local_maps=True)
+    for pb in (a, b):  # change the material between calls (rho -> 1.5 rho)
+        pb.datasets["mat"].values.view(-1, pb.datasets["mat"].values_per_element)[:, 0] *= 1.5
+    for _ in range(2):
+        lt.execute_schedule(sa, a.chain, a.bindings, a.datasets, a.registry, use_local_maps=True)
+    runner()
+    for n in ("u", "s", "ru", "rs"):
+        np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
