@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (nx, ny, p, steps_per_chain, chains_per_job, material, ts, renumber)
-    2: dict(nx=256, ny=256, p=1, T=1, chains=10, material="homogeneous", ts=32,
+    2: dict(nx=256, ny=256, p=1, T=1, chains=10, material="homogeneous", ts=28,
             workload="elastic DG P1 256x256 (131072 cells), 1 timestep/chain, 10 timesteps"),
     3: dict(nx=2048, ny=2048, p=2, T=2, chains=1, material=("uniform", 2), ts=24,
             workload="elastic DG P2 2048x2048 (8.4M cells), 2 timesteps/chain, heterogeneous"),
@@ -252,6 +252,31 @@ def run_partitioned(args, cfg, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
     dev_s = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) * 1e-3, world)
+    launches_per_step = launches[0] // max(args.warmup + args.steps, 1)
+    # end to end: H2D of the rank's u,s (pinned), the step, D2H of u,s
+    e2e_s = None
+    if not args.no_e2e:
+        host = {n: torch.empty(pb.datasets[n].values.numel(), dtype=torch.float64,
+                               pin_memory=True) for n in ("u", "s")}
+        for n in host:
+            host[n].copy_(pb.datasets[n].values)
+        h2d = sum(h.numel() * 8 for h in host.values())
+        e2e_ev = []
+        torch.cuda.synchronize()
+        barrier(world)
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for n in host:
+                pb.datasets[n].values.copy_(host[n], non_blocking=True)
+            step()
+            for n in host:
+                host[n].copy_(pb.datasets[n].values, non_blocking=True)
+            b.record(stream)
+            e2e_ev.append((a, b))
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(sum(a.elapsed_time(b) for a, b in e2e_ev) * 1e-3, world)
     owned = lm.sizes["cells"].owned_total
     owned_dofs = owned * 5 * (cfg["p"] + 1) * (cfg["p"] + 2) // 2
     total_dofs = owned_dofs
@@ -262,10 +287,13 @@ def run_partitioned(args, cfg, rank, world, local):
         total_dofs = int(tdofs.item())
     updates = total_dofs * T * cfg["chains"] * args.steps
     value = updates / dev_s
+    e2e = None
+    if e2e_s is not None:
+        e2e = {"value": total_dofs * T * cfg["chains"] * len(e2e_ev) / e2e_s,
+               "unit": "DoF-updates/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d}
     totals = {n: loc.spaces[loc.space_of[n]].total for n in loc.vpe}
     b_chain = compulsory_bytes(pb.chain, pb.bindings, dict(loc.vpe), totals)
     peak, peak_kind = measured_peaks()
-    launches_per_step = launches[0] // max(args.warmup + args.steps, 1)
     achieved = b_chain * world * cfg["chains"] * args.steps / dev_s / 1e9
     if rank == 0:
         print(json.dumps({
@@ -288,7 +316,7 @@ def run_partitioned(args, cfg, rank, world, local):
                          "unit": "GB/s", "frac": achieved / (peak * world), "traffic": None,
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_chain_rank0": b_chain},
-            "cpu_baseline": None, "e2e": None,
+            "cpu_baseline": None, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }))

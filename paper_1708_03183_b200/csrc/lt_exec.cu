@@ -605,6 +605,20 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       const int which = (L.kernel - K_DG_FIRST) % 5;
       if (FAM >= 1 && FAM <= 4 && L.kernel >= K_DG_FIRST) {  // kernel selected once per loop
         constexpr int PP = FAM >= 1 && FAM <= 4 ? FAM : 1;
+        if (which == 3 && L.nobar == 2 && (P.loops[j + 1].kernel - K_DG_FIRST) % 5 == 4) {
+          // inverse mass and update over the same items, lane-local: one pass
+          const DLoop &L2 = P.loops[j + 1];
+          const int *LH2 = B + P.loop_pos[j + 1];
+          for_items_s(n, L, [&](int pos, int lane) {
+            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            dg_minv<PP>(cx, lane);
+            StagedCtx cy{L2, 0, pos, 0, smem, scratch, base, B, LH2 + 2};
+            dg_axpy<PP>(cy, lane);
+          });
+          ++j;
+          if (!L2.nobar || (j + 1 < P.n_loops && B[P.loop_pos[j + 1]] == 0)) __syncthreads();
+          continue;
+        }
         if (which == 0)
           for_items_s(n, L, [&](int pos, int lane) {
             StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
@@ -1632,8 +1646,10 @@ __global__ void k_differs(const int32_t *a, const int32_t *b, int64_t n, int32_t
 //  (b) loop j+1's first phase (its body; INC bodies write only scratch) neither
 //      reads nor writes a dataset loop j writes, and writes nothing loop j
 //      reads (DG volume -> interior-facet records).
-static bool barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &cv,
-                              const lt_arg *args, int j) {
+// 0: loop j+1 needs a barrier after loop j; 1: independent datasets; 2: same
+// items and lane-local kernels (the executor may run both bodies per item)
+static int barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &cv,
+                             const lt_arg *args, int j) {
   const LoopDesc &A = cv.loops[j], &Bq = cv.loops[j + 1];
   for (const lt_desc &d : A.desc)
     if (d.map >= 0 && d.mode != LT_READ) return false;  // loop j must not have an apply phase
@@ -1652,7 +1668,7 @@ static bool barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &c
       if (!a_writes && b_body_writes) indep = false;
     }
   }
-  if (indep) return true;
+  if (indep) return 1;
   // (a) same items, lane-local kernels
   auto lane_local = [](int k) {
     return k >= K_DG_FIRST && ((k - K_DG_FIRST) % 5 == 3 || (k - K_DG_FIRST) % 5 == 4);
@@ -1676,7 +1692,7 @@ static bool barrier_free_pair(Ctx &ctx, const lt_schedule *s, const ChainView &c
   int32_t f = 1;
   LT_CK(cudaMemcpyAsync(&f, flag.get(), 4, cudaMemcpyDeviceToHost, ctx.stream));
   LT_CK(cudaStreamSynchronize(ctx.stream));
-  return f == 0;
+  return f == 0 ? 2 : 0;
 }
 
 __global__ void k_u8_to_i32(const uint8_t *a, int64_t n, int32_t *b) {
@@ -2327,7 +2343,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
     for (int j = 0; j + 1 < nl; ++j)
-      P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j) ? 1 : 0;
+      P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j);
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
     const size_t blob_max = build_blobs(ctx, s, cv, P, sp_index, ds_space);
     H.blob = P.blob.get();
@@ -2340,6 +2356,8 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       return nullptr;
     }
     P.smem_bytes = blob_max + P.data_max + scratch_max;
+    if (const char *pad = getenv("LT_SMEM_PAD_KB"))  // diagnostics: force lower occupancy
+      P.smem_bytes = std::min(kSmemMax, P.smem_bytes + 1024 * (size_t)atoi(pad));
     if (getenv("LT_DEBUG_PLAN")) print_plan_stats(s, P, blob_max, scratch_max);
     if (P.dataflow) build_dependencies(ctx, s, P);
   } else {

@@ -109,7 +109,8 @@ struct DLoop {
   int32_t lane_dq, lane_dr; // LT_SBLOCK / lanes, LT_SBLOCK % lanes
   uint32_t row_magic;       // deferred apply: lt_magic(rows per target)
   int32_t row_dq, row_dr;   // LT_SBLOCK / rows, LT_SBLOCK % rows
-  int32_t nobar;            // staged: no barrier before the next loop (same items, lane-local)
+  int32_t nobar;            // staged: no barrier before the next loop (1: independent data,
+                            // 2: same items, lane-local kernels -- fused per item)
   const double *params;
   const int32_t *offsets;   // tiled: per-tile list offsets
   const int32_t *elements;  // tiled: concatenated lists
