@@ -427,6 +427,33 @@ __device__ __forceinline__ void apply_plan(const DLoop &L, int p, const int *gc_
 // consecutive threads copy consecutive components of a row (coalesced within
 // rows and along runs of consecutive ids), and the loop carries no division
 // or component wrap-around (4-5 instructions per copy).
+// no "memory" clobber: the index loads may move across the copies (the rows
+// they fill are read only after cp_async_wait_all + a barrier)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_nc(double *smem_dst, const double *gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  if (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src));
+}
+
+template <int BYTES>
+__device__ __forceinline__ void gather_loop(const double *__restrict__ src, double *dst,
+                                            const int *__restrict__ idx, int i, int n, int rpp,
+                                            int step, uint32_t v, uint32_t c) {
+  // four rows per trip: their index loads are independent and overlap
+  for (; i + 3 * rpp < n; i += 4 * rpp, dst += 4 * step) {
+    const uint32_t g0 = (uint32_t)idx[i], g1 = (uint32_t)idx[i + rpp];
+    const uint32_t g2 = (uint32_t)idx[i + 2 * rpp], g3 = (uint32_t)idx[i + 3 * rpp];
+    cp_async_nc<BYTES>(dst, src + (g0 * v + c));
+    cp_async_nc<BYTES>(dst + step, src + (g1 * v + c));
+    cp_async_nc<BYTES>(dst + 2 * step, src + (g2 * v + c));
+    cp_async_nc<BYTES>(dst + 3 * step, src + (g3 * v + c));
+  }
+  for (; i < n; i += rpp, dst += step) cp_async_nc<BYTES>(dst, src + ((uint32_t)idx[i] * v + c));
+}
+
 __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, double *rows) {
   const uint32_t v = (uint32_t)S.vpe;
   const int rpp = S.di;
@@ -436,40 +463,37 @@ __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, doub
   const int r0 = lt_div(threadIdx.x, unit, S.magic);
   if (r0 >= rpp) return;
   const uint32_t c = (uint32_t)(threadIdx.x - r0 * unit) << S.vec;  // thread's first double
-  const double *src = S.data;
   double *dst = rows + r0 * S.stride + c;
   const int step = rpp * S.stride;
-  if (S.vec) {  // 16-byte pairs: even rows, 16-byte aligned in HBM and shared memory
-    for (int i = r0; i < nrow; i += rpp, dst += step) cp_async16(dst, src + ((uint32_t)idx[i] * v + c));
-    return;
-  }
-  for (int i = r0; i < nrow; i += rpp, dst += step) cp_async8(dst, src + ((uint32_t)idx[i] * v + c));
+  if (S.vec)  // 16-byte pairs: even rows, 16-byte aligned in HBM and shared memory
+    gather_loop<16>(S.data, dst, idx, r0, nrow, rpp, step, v, c);
+  else
+    gather_loop<8>(S.data, dst, idx, r0, nrow, rpp, step, v, c);
 }
 
 // Store back the rows of dataset S the tile wrote (compact list wl of
-// footprint positions), same thread mapping as the gather.  Rows go in batches
-// of SB: all shared-memory loads of a batch are issued before its
-// global stores (the stores may alias nothing the loads read, but the compiler
-// cannot know), so the wl -> idx -> row load chains overlap.
+// footprint positions), same thread mapping as the gather.  SB = 2: two rows
+// per trip with both rows' shared-memory loads issued before the global
+// stores, so the wl -> idx -> row load chains overlap.
 template <int SB, class T>
-__device__ __forceinline__ void store_rows_t(double *dst, const double *src, const int *idx,
-                                            const int *wl, int nw, int r0, int rpp, uint32_t v,
-                                            int sv) {
-  for (int i = r0; i < nw; i += SB * rpp) {
-    int r[SB];
-    uint32_t g[SB];
-    T x[SB];
-#pragma unroll
-    for (int k = 0; k < SB; ++k) r[k] = i + k * rpp < nw ? wl[i + k * rpp] : -1;
-#pragma unroll
-    for (int k = 0; k < SB; ++k)
-      if (r[k] >= 0) {
-        g[k] = (uint32_t)idx[r[k]] * v;
-        x[k] = *reinterpret_cast<const T *>(src + r[k] * sv);
-      }
-#pragma unroll
-    for (int k = 0; k < SB; ++k)
-      if (r[k] >= 0) *reinterpret_cast<T *>(dst + g[k]) = x[k];
+__device__ __forceinline__ void store_rows_t(double *__restrict__ dst,
+                                            const double *__restrict__ src,
+                                            const int *__restrict__ idx,
+                                            const int *__restrict__ wl, int nw, int r0, int rpp,
+                                            uint32_t v, int sv) {
+  int i = r0;
+  if (SB >= 2)
+    for (; i + rpp < nw; i += 2 * rpp) {  // two rows per trip, loads before stores
+      const int ra = wl[i], rb = wl[i + rpp];
+      const uint32_t ga = (uint32_t)idx[ra] * v, gb = (uint32_t)idx[rb] * v;
+      const T xa = *reinterpret_cast<const T *>(src + ra * sv);
+      const T xb = *reinterpret_cast<const T *>(src + rb * sv);
+      *reinterpret_cast<T *>(dst + ga) = xa;
+      *reinterpret_cast<T *>(dst + gb) = xb;
+    }
+  for (; i < nw; i += rpp) {
+    const int r = wl[i];
+    *reinterpret_cast<T *>(dst + (uint32_t)idx[r] * v) = *reinterpret_cast<const T *>(src + r * sv);
   }
 }
 
@@ -798,7 +822,7 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
     __syncthreads();
     LT_TACC(3, t_wait);
     LT_TSTAMP(t_tile);
-    run_tile<FAM, (MINB >= 7 ? 1 : 4)>(P, t, smem, base);
+    run_tile<FAM, 2>(P, t, smem, base);
     prev = t;
     LT_TACC(4, t_tile);
 #ifdef LT_PHASE_TIMING
@@ -2397,6 +2421,9 @@ static StagedFn staged_fn(int fam) {
 }
 
 typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
+#ifndef LT_NARROW_MINB
+#define LT_NARROW_MINB 7  // CTAs per SM of the narrow (72-register at 128 threads) build
+#endif
 static DataflowFn dataflow_fn(int fam, bool wide = false) {
   if (wide) switch (fam) {
       case 1: return k_dataflow<1, 4>;
@@ -2406,12 +2433,12 @@ static DataflowFn dataflow_fn(int fam, bool wide = false) {
       default: break;
     }
   switch (fam) {
-    case 0: return k_dataflow<0, 7>;
-    case 1: return k_dataflow<1, 7>;
-    case 2: return k_dataflow<2, 7>;
-    case 3: return k_dataflow<3, 7>;
-    case 4: return k_dataflow<4, 7>;
-    default: return k_dataflow<5, 7>;
+    case 0: return k_dataflow<0, LT_NARROW_MINB>;
+    case 1: return k_dataflow<1, LT_NARROW_MINB>;
+    case 2: return k_dataflow<2, LT_NARROW_MINB>;
+    case 3: return k_dataflow<3, LT_NARROW_MINB>;
+    case 4: return k_dataflow<4, LT_NARROW_MINB>;
+    default: return k_dataflow<5, LT_NARROW_MINB>;
   }
 }
 
