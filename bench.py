@@ -460,6 +460,7 @@ def main():
                        "colors": len(sched.color_order), "rounds": sched.recolor_rounds,
                        "inspect_s": round(inspect_s, 4),
                        "executor": "untiled" if args.untiled else runner.executor,
+                       "queue_order": None if args.untiled else runner.queue_order,
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LT_ABI_VERSION 1
+#define LT_ABI_VERSION 2
 
 /* status codes (errors.py:4-33) */
 #define LT_OK                 0
@@ -140,6 +140,7 @@ typedef struct {
     int64_t elements;    /* element visits (sum over loops) */
     int32_t staged;      /* 0: global-memory tiles, 1: staged per colour, 2: staged dataflow */
     int32_t smem_bytes;  /* dynamic shared memory per CTA */
+    int32_t wave_order;  /* dataflow queue: 1 wavefront (L2-local) order, 0 colour-major */
 } lt_exec_info;
 
 /* ---- library / context ---------------------------------------------------- */

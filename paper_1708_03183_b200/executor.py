@@ -333,6 +333,8 @@ class TiledRunner:
         self.launches_per_call = info.launches
         self.executor = {0: "global", 1: "staged", 2: "dataflow"}[info.staged]
         self.smem_bytes = info.smem_bytes
+        self.queue_order = ("wavefront" if info.wave_order else "colour-major") \
+            if info.staged == 2 else None
 
     def __call__(self):
         """Execute the chain ``repeats`` times (one persistent launch when dataflow)."""

@@ -111,3 +111,25 @@ def test_gpu_dg_repeat_repacks_constants_each_call(p, steps):
     runner()
     for n in ("u", "s", "ru", "rs"):
         np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
+
+
+@pytest.mark.parametrize("order", ["wave", "colour"])
+def test_gpu_dg_queue_orders_equal_sequential_calls(order, monkeypatch):
+    """The dataflow queue order (wavefront or colour-major) never changes
+    results: repeated execution is bitwise equal to sequential calls."""
+    from paper_1708_03183_b200.dg import elastic_setup
+    from paper_1708_03183_b200.executor import TiledRunner
+    monkeypatch.setenv("LT_ORDER", order)
+    mk = lambda: elastic_problem(elastic_setup(44, 36, 2, 2, material=("uniform", 7), sigma=5.0))
+    a, b = mk(), mk()
+    a.install_params()
+    sa = lt.inspect_chain(a.chain, 16, lt.ExecMode.SHARED)
+    for _ in range(4):
+        lt.execute_schedule(sa, a.chain, a.bindings, a.datasets, a.registry, use_local_maps=True)
+    sb = lt.inspect_chain(b.chain, 16, lt.ExecMode.SHARED)
+    r = TiledRunner(sb, b.chain, b.bindings, b.datasets, b.registry, repeats=2)
+    if r.executor == "dataflow":
+        assert r.queue_order == ("wavefront" if order == "wave" else "colour-major")
+    r()
+    for n in ("u", "s", "ru", "rs"):
+        np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)

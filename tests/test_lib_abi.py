@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_kernel_table():
     lib = _lib.load()
-    assert lib.lt_abi_version() == 1
+    assert lib.lt_abi_version() == 2
     names = _lib.kernel_names()
     for k in ("edge_inc", "cell_inc", "edge_read", "cell_read", "toy_k1", "toy_k2", "toy_k3"):
         assert k in names
