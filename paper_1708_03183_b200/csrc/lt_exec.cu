@@ -641,6 +641,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
           });
           ++j;
           if (!L2.nobar || (j + 1 < P.n_loops && B[P.loop_pos[j + 1]] == 0)) __syncthreads();
+          LT_TACC(8 + (j < 24 ? j : 23), t_loop);
           continue;
         }
         if (which == 0)
