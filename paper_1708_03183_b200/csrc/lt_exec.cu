@@ -329,7 +329,7 @@ struct StagedParams {
   int32_t ds_pos;                    // header position of the written-row lists
   int32_t prog_pos;                  // header position of the program length (ints)
   int32_t ro_packed;                 // rows of read-only datasets follow the program in the blob
-  int32_t pad;
+  int32_t dep_pos;                   // header position of the dependency list (dataflow)
   const int32_t *blob;
   const int64_t *blob_off;           // per tile: first int of its blob
   const int32_t *blob_len;           // per tile: ints (multiple of 4)
@@ -753,8 +753,6 @@ struct DataflowArgs {
   const int32_t *item_t;   // per queue item: tile
   const int32_t *item_k;   // per queue item: repeat
   const int32_t *order;    // executable tiles in queue order
-  const int32_t *nbr_off;  // per tile: range in nbr
-  const int32_t *nbr;      // (tile << 1) | earlier-colour flag; includes the tile itself
   int32_t *done;           // per tile: completed repeats
   int32_t *queue;          // next item
   int32_t n_exec;
@@ -812,12 +810,16 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
     }
     tile_prefetch(P, t, smem, base, &bar, phase, true);  // overlaps the dependency wait
     phase ^= 1u;
-    const int n0 = D.nbr_off[t], n1 = D.nbr_off[t + 1];
     LT_TSTAMP(t_wait);
-    // ld.acquire.gpu also invalidates this SM's L1 (CCTL.IVALL), so the
-    // gathers below cannot see stale lines of rows other tiles wrote
-    for (int i = n0 + threadIdx.x; i < n1; i += LT_SBLOCK) {
-      const int e = D.nbr[i];
+    // the tile's dependency list arrived with its program (one global round
+    // trip per wait: the done counter).  ld.acquire.gpu also invalidates this
+    // SM's L1 (CCTL.IVALL), so the gathers below cannot see stale lines of
+    // rows other tiles wrote
+    const int *Bt = reinterpret_cast<const int *>(smem);
+    const int n_dep = Bt[P.dep_pos];
+    const int *dep = Bt + Bt[P.dep_pos + 1];
+    for (int i = threadIdx.x; i < n_dep; i += LT_SBLOCK) {
+      const int e = dep[i];
       const int need = k + (e & 1);
       const int32_t *flag = D.done + (e >> 1);
       while (ld_acquire(flag) < need) __nanosleep(32);
@@ -1854,6 +1856,8 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   H.ds_pos = hp;
   hp += 2 * H.n_ds;
   H.prog_pos = hp++;
+  H.dep_pos = hp;  // dataflow: (count, position) of the tile's dependency list
+  hp += 2;
   H.hs = hp;
   // host copies of the per-tile ranges
   std::vector<std::vector<int32_t>> off(nl), cb(nl);
@@ -1904,6 +1908,8 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   }
   for (int k = 0; k < H.n_ds; ++k)
     if (P.wflags[k].get()) s_wf[k] = (int)secs.size(), sec(P.wlist[k].get(), false);
+  const int s_dep = P.dataflow ? (int)secs.size() : -1;
+  if (P.dataflow) sec(P.nbr.get(), false);
   std::vector<int32_t> hdr(H.hs);
   int n_exec = 0;
   for (int t = 0; t < nt; ++t) {
@@ -1963,6 +1969,12 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       const int32_t o = P.wbeg[k][t], n = P.wbeg[k][t + 1] - o;
       hdr[H.ds_pos + 2 * k] = n;
       hdr[H.ds_pos + 2 * k + 1] = put(s_wf[k], o, n, 0);
+    }
+    hdr[H.dep_pos] = 0;
+    if (s_dep >= 0) {
+      const int32_t o = P.nbr_off_host[t], n = P.nbr_off_host[t + 1] - o;
+      hdr[H.dep_pos] = n;
+      hdr[H.dep_pos + 1] = put(s_dep, o, n, 0);
     }
     cur = (cur + 3) / 4 * 4;  // 16-byte aligned programs
     hdr[H.prog_pos] = (int32_t)cur;
@@ -2477,6 +2489,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     for (int j = 0; j + 1 < nl; ++j)
       P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j);
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
+    if (P.dataflow) build_dependencies(ctx, s, P);  // tile programs carry the lists
     const size_t blob_max = build_blobs(ctx, s, cv, P, sp_index, ds_space);
     H.blob = P.blob.get();
     H.blob_off = P.blob_off.get();
@@ -2491,7 +2504,6 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     if (const char *pad = getenv("LT_SMEM_PAD_KB"))  // diagnostics: force lower occupancy
       P.smem_bytes = std::min(kSmemMax, P.smem_bytes + 1024 * (size_t)atoi(pad));
     if (getenv("LT_DEBUG_PLAN")) print_plan_stats(s, P, blob_max, scratch_max);
-    if (P.dataflow) build_dependencies(ctx, s, P);
   } else {
     P.smem_bytes = scratch_max;
   }
@@ -2619,8 +2631,6 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       D.item_k = its.second.get();
       if (info) info->wave_order = P.items_wave.at({kind, repeats});
     }
-    D.nbr_off = P.nbr_off.get();
-    D.nbr = P.nbr.get();
     D.done = P.done.get();
     D.queue = P.queue.get();
     if (core)  // a boundary-only call continues the counters of its core call
