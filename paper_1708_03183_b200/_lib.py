@@ -77,7 +77,8 @@ class LtScheduleInfo(C.Structure):
 
 class LtExecInfo(C.Structure):
     _fields_ = [("launches", C.c_int32), ("n_colors", C.c_int32), ("elements", C.c_int64),
-                ("staged", C.c_int32), ("smem_bytes", C.c_int32), ("wave_order", C.c_int32)]
+                ("staged", C.c_int32), ("smem_bytes", C.c_int32), ("wave_order", C.c_int32),
+                ("wide_build", C.c_int32)]
 
 
 # every symbol the header declares, with (restype, argtypes)

@@ -2541,15 +2541,18 @@ static StagedFn staged_fn(int fam) {
 }
 
 typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
+#ifndef LT_WIDE_MINB
+#define LT_WIDE_MINB 4  // CTAs per SM of the wide (128-register at 128 threads) build
+#endif
 #ifndef LT_NARROW_MINB
 #define LT_NARROW_MINB 7  // CTAs per SM of the narrow (72-register at 128 threads) build
 #endif
 static DataflowFn dataflow_fn(int fam, bool wide = false) {
   if (wide) switch (fam) {
-      case 1: return k_dataflow<1, 4>;
-      case 2: return k_dataflow<2, 4>;
-      case 3: return k_dataflow<3, 4>;
-      case 4: return k_dataflow<4, 4>;
+      case 1: return k_dataflow<1, LT_WIDE_MINB>;
+      case 2: return k_dataflow<2, LT_WIDE_MINB>;
+      case 3: return k_dataflow<3, LT_WIDE_MINB>;
+      case 4: return k_dataflow<4, LT_WIDE_MINB>;
       default: break;
     }
   switch (fam) {
@@ -2595,7 +2598,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       LT_CK(cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)P.smem_bytes));
     LT_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, narrow, LT_SBLOCK, P.smem_bytes));
-    P.wide = per_sm <= 4 && fam >= 1 && fam <= 4 && !getenv("LT_NARROW");
+    P.wide = per_sm <= LT_WIDE_MINB && fam >= 1 && fam <= 4 && !getenv("LT_NARROW");
     if (P.wide) {
       const void *w = (const void *)dataflow_fn(fam, true);
       if (P.smem_bytes > 48 * 1024)
@@ -2629,7 +2632,10 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       auto &its = P.items.at({kind, repeats});
       D.item_t = its.first.get();
       D.item_k = its.second.get();
-      if (info) info->wave_order = P.items_wave.at({kind, repeats});
+      if (info) {
+        info->wave_order = P.items_wave.at({kind, repeats});
+        info->wide_build = P.wide ? 1 : 0;
+      }
     }
     D.done = P.done.get();
     D.queue = P.queue.get();

@@ -335,6 +335,7 @@ class TiledRunner:
         self.smem_bytes = info.smem_bytes
         self.queue_order = ("wavefront" if info.wave_order else "colour-major") \
             if info.staged == 2 else None
+        self.wide_build = bool(info.wide_build)
 
     def __call__(self):
         """Execute the chain ``repeats`` times (one persistent launch when dataflow)."""

@@ -133,3 +133,20 @@ def test_gpu_dg_queue_orders_equal_sequential_calls(order, monkeypatch):
     r()
     for n in ("u", "s", "ru", "rs"):
         np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
+
+
+def test_gpu_dg_wide_register_build_matches_untiled():
+    """P2 two-step tiles large enough that shared memory allows <= 4 CTAs per
+    SM run the 128-register dataflow build; results equal the untiled path."""
+    from paper_1708_03183_b200.dg import elastic_setup
+    from paper_1708_03183_b200.executor import TiledRunner
+    mk = lambda: elastic_problem(elastic_setup(64, 48, 2, 2, material=("uniform", 9), sigma=6.0))
+    a, b = mk(), mk()
+    a.run_untiled(n_chains=3)
+    s = lt.inspect_chain(b.chain, 32, lt.ExecMode.SHARED)
+    b.install_params()
+    r = TiledRunner(s, b.chain, b.bindings, b.datasets, b.registry, repeats=3)
+    if r.executor == "dataflow":
+        assert r.wide_build, r.smem_bytes
+    for n in ("u", "s"):
+        assert rel_err(b.datasets[n].numpy(), a.datasets[n].numpy()) <= RTOL, n
