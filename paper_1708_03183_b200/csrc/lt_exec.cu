@@ -759,6 +759,9 @@ struct DataflowArgs {
   int32_t n_items;
 };
 
+#ifndef LT_POLL_NS
+#define LT_POLL_NS 32  // back-off between polls of an unfinished dependency
+#endif
 __device__ __forceinline__ int ld_acquire(const int32_t *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -783,13 +786,12 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
   // held by running CTAs and the schedule stays deadlock-free
   int next = threadIdx.x == 0 ? atomicAdd(D.queue, 1) : 0;
   int prev = -1;  // tile whose completion is still to be released
-  // release: the barrier below orders every thread's store-back before thread
-  // 0's cumulative gpu-scope fence + increment (CUTLASS GenericBarrier's
-  // arrive); it is issued after the next tile program's TMA so the fence
-  // latency overlaps that load
+  // release: the barrier at the top of the loop orders every thread's
+  // store-back before thread 0's cumulative gpu-scope release increment
+  // (CUTLASS GenericBarrier's arrive); it is issued after the next tile
+  // program's TMA so its latency overlaps that load
   auto release = [&](int tile) {
-    asm volatile("fence.acq_rel.gpu;\nred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(D.done + tile)
-                 : "memory");
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(D.done + tile) : "memory");
   };
   for (;;) {
     if (threadIdx.x == 0) {
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
       const int e = dep[i];
       const int need = k + (e & 1);
       const int32_t *flag = D.done + (e >> 1);
-      while (ld_acquire(flag) < need) __nanosleep(32);
+      while (ld_acquire(flag) < need) __nanosleep(LT_POLL_NS);
     }
     __syncthreads();
     LT_TACC(3, t_wait);
