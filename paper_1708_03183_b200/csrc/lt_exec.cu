@@ -579,7 +579,6 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
 // memory, store back the rows this tile wrote.
 template <int FAM, int SB = 1>
 __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base) {
-  const int tid = threadIdx.x;
   const int *B = reinterpret_cast<const int *>(smem);
   LT_TSTAMP(t_gather);
   for (int d = 0; d < P.n_ds; ++d)
@@ -1698,73 +1697,6 @@ static void to_host(Ctx &ctx, const DevBuf<T> &d, int64_t n, std::vector<T> &h) 
   if (n) LT_CK(cudaMemcpyAsync(h.data(), d.get(), sizeof(T) * n, cudaMemcpyDeviceToHost, ctx.stream));
 }
 
-// Runs of consecutive global ids inside each tile's footprint (optionally only
-// over flagged entries): the unit of the coalesced gather / store-back.
-__global__ void k_run_marks(const int32_t *elem, const uint32_t *tile, const uint8_t *flag,
-                            int64_t n, int32_t *head, int32_t *tail) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const bool on = flag ? flag[i] != 0 : true;
-  const bool cont_prev = i > 0 && tile[i - 1] == tile[i] && elem[i - 1] + 1 == elem[i] &&
-                         (flag ? flag[i - 1] != 0 : true);
-  const bool cont_next = i + 1 < n && tile[i + 1] == tile[i] && elem[i] + 1 == elem[i + 1] &&
-                         (flag ? flag[i + 1] != 0 : true);
-  head[i] = on && !cont_prev;
-  tail[i] = on && !cont_next;
-}
-
-__global__ void k_run_emit(const int32_t *elem, const uint32_t *tile, const int32_t *fp_off,
-                           const int32_t *head, const int32_t *tail, const int32_t *hidx,
-                           const int32_t *tidx, int64_t n, int32_t *runs3, uint32_t *run_tile) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (head[i]) {
-    const int r = hidx[i];
-    runs3[3 * r] = (int32_t)(i - fp_off[tile[i]]);
-    runs3[3 * r + 1] = elem[i];
-    run_tile[r] = tile[i];
-    atomicAdd(&runs3[3 * r + 2], -(int32_t)i);
-  }
-  if (tail[i]) atomicAdd(&runs3[3 * tidx[i] + 2], (int32_t)i + 1);
-}
-
-struct RunSet {
-  DevBuf<int32_t> runs3;  // (tile-local first row, first global id, length) per run
-  DevBuf<int32_t> off;    // per tile: range of runs
-  std::vector<int32_t> off_host;
-};
-
-static void build_runs(Ctx &ctx, const Footprint &fp, const uint8_t *flag, int n_tiles,
-                       RunSet &out) {
-  const int64_t n = fp.n;
-  DevBuf<int32_t> head(std::max<int64_t>(n, 1), ctx.stream), tail(std::max<int64_t>(n, 1), ctx.stream),
-      hidx(std::max<int64_t>(n, 1), ctx.stream), tidx(std::max<int64_t>(n, 1), ctx.stream);
-  int64_t R = 0;
-  if (n) {
-    k_run_marks<<<grid_for(n, 256), 256, 0, ctx.stream>>>(fp.elem.get(), fp.tile.get(), flag, n,
-                                                         head.get(), tail.get());
-    LT_CK_LAUNCH();
-    exclusive_sum(ctx, head.get(), hidx.get(), n);
-    exclusive_sum(ctx, tail.get(), tidx.get(), n);
-    R = last_plus(ctx, hidx.get(), head.get(), n);
-  }
-  out.runs3.alloc(std::max<int64_t>(3 * R, 3), ctx.stream);
-  LT_CK(cudaMemsetAsync(out.runs3.get(), 0, 4 * out.runs3.n, ctx.stream));
-  DevBuf<uint32_t> rt(std::max<int64_t>(R, 1), ctx.stream);
-  if (n) {
-    k_run_emit<<<grid_for(n, 256), 256, 0, ctx.stream>>>(fp.elem.get(), fp.tile.get(),
-                                                        fp.off.get(), head.get(), tail.get(),
-                                                        hidx.get(), tidx.get(), n, out.runs3.get(),
-                                                        rt.get());
-    LT_CK_LAUNCH();
-  }
-  out.off.alloc(n_tiles + 1, ctx.stream);
-  lower_bound_u32(ctx, rt.get(), R, n_tiles, out.off.get());
-  out.off_host.resize(n_tiles + 1);
-  LT_CK(cudaMemcpyAsync(out.off_host.data(), out.off.get(), 4 * (n_tiles + 1),
-                        cudaMemcpyDeviceToHost, ctx.stream));
-  LT_CK(cudaStreamSynchronize(ctx.stream));
-}
 
 __global__ void k_differs(const int32_t *a, const int32_t *b, int64_t n, int32_t *flag) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
