@@ -27,18 +27,19 @@ namespace lt {
 
 // ---- kernel table -------------------------------------------------------------
 // signature tokens per descriptor: D* direct any, DR direct read, DW direct
-// write/rw, MR mapped read, MI mapped inc (or write)
+// write/rw, DF direct write of every component (a WRITE binding then needs no
+// load of the rows it writes), MR mapped read, MI mapped inc (or write)
 struct KernelSpec {
   const char *name;
   const char *sig;
 };
 
 static const KernelSpec kSpecs[] = {
-    {"edge_inc", "D*,MI"},  {"cell_inc", "D*,MI"},  {"edge_read", "DW,MR"},
-    {"cell_read", "DW,MR"}, {"toy_k1", "D*,MI"},    {"toy_k2", "DW,MR"},
+    {"edge_inc", "D*,MI"},  {"cell_inc", "D*,MI"},  {"edge_read", "DF,MR"},
+    {"cell_read", "DF,MR"}, {"toy_k1", "D*,MI"},    {"toy_k2", "DF,MR"},
     {"toy_k3", "DW,MR"},
 #define LT_DG_SPEC(P)                                                                  \
-  {"dg_vol_p" #P, "DR,DR,DR,DR,DW,DW"}, {"dg_iflux_p" #P, "DR,MR,MR,MR,MI,MI"},        \
+  {"dg_vol_p" #P, "DR,DR,DR,DR,DF,DF"}, {"dg_iflux_p" #P, "DR,MR,MR,MR,MI,MI"},        \
       {"dg_eflux_p" #P, "DR,MR,MR,MR,MI,MI"}, {"dg_minv_p" #P, "DR,DR,DW,DW"},         \
       {"dg_axpy_p" #P, "DW,DW,DR,DR"}
     LT_DG_SPEC(1), LT_DG_SPEC(2), LT_DG_SPEC(3), LT_DG_SPEC(4),
@@ -330,6 +331,8 @@ struct StagedParams {
   int32_t prog_pos;                  // header position of the program length (ints)
   int32_t ro_packed;                 // rows of read-only datasets follow the program in the blob
   int32_t dep_pos;                   // header position of the dependency list (dataflow)
+  int32_t ld_pos;                    // header position of the per-dataset load lists
+  int32_t pad;
   const int32_t *blob;
   const int64_t *blob_off;           // per tile: first int of its blob
   const int32_t *blob_len;           // per tile: ints (multiple of 4)
@@ -471,6 +474,39 @@ __device__ __forceinline__ void gather_rows(const StageDS &S, const int *B, doub
     gather_loop<8>(S.data, dst, idx, r0, nrow, rpp, step, v, c);
 }
 
+// Gather only the listed footprint rows (load == 2: rows the first writer of
+// the dataset does not overwrite), same thread mapping.
+__device__ __forceinline__ void gather_rows_listed(const StageDS &S, const int *B, const int *ll,
+                                                   int nl, double *rows) {
+  const uint32_t v = (uint32_t)S.vpe;
+  const int rpp = S.di;
+  const int *idx = B + B[2 * S.sp + 1];
+  const int unit = S.vec ? (int)v >> 1 : (int)v;
+  const int r0 = lt_div(threadIdx.x, unit, S.magic);
+  if (r0 >= rpp) return;
+  const uint32_t c = (uint32_t)(threadIdx.x - r0 * unit) << S.vec;
+  double *dst = rows + c;
+  int i = r0;
+  for (; i + rpp < nl; i += 2 * rpp) {  // two rows per trip: list and index loads overlap
+    const int ra = ll[i], rb = ll[i + rpp];
+    const uint32_t ga = (uint32_t)idx[ra], gb = (uint32_t)idx[rb];
+    if (S.vec) {
+      cp_async_nc<16>(dst + ra * S.stride, S.data + (ga * v + c));
+      cp_async_nc<16>(dst + rb * S.stride, S.data + (gb * v + c));
+    } else {
+      cp_async_nc<8>(dst + ra * S.stride, S.data + (ga * v + c));
+      cp_async_nc<8>(dst + rb * S.stride, S.data + (gb * v + c));
+    }
+  }
+  for (; i < nl; i += rpp) {
+    const int r = ll[i];
+    if (S.vec)
+      cp_async_nc<16>(dst + r * S.stride, S.data + ((uint32_t)idx[r] * v + c));
+    else
+      cp_async_nc<8>(dst + r * S.stride, S.data + ((uint32_t)idx[r] * v + c));
+  }
+}
+
 // Store back the rows of dataset S the tile wrote (compact list wl of
 // footprint positions), same thread mapping as the gather.  SB = 2: two rows
 // per trip with both rows' shared-memory loads issued before the global
@@ -581,8 +617,14 @@ template <int FAM, int SB = 1>
 __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base) {
   const int *B = reinterpret_cast<const int *>(smem);
   LT_TSTAMP(t_gather);
-  for (int d = 0; d < P.n_ds; ++d)
-    if (P.ds[d].load && !P.ds[d].ro) gather_rows(P.ds[d], B, smem + base[d]);
+  for (int d = 0; d < P.n_ds; ++d) {
+    const StageDS &S = P.ds[d];
+    if (S.ro || !S.load) continue;
+    if (S.load == 2)
+      gather_rows_listed(S, B, B + B[P.ld_pos + 2 * d + 1], B[P.ld_pos + 2 * d], smem + base[d]);
+    else
+      gather_rows(S, B, smem + base[d]);
+  }
   cp_async_wait_all();
   __syncthreads();
   LT_TACC(1, t_gather);
@@ -1170,6 +1212,8 @@ struct ExecPlan {
   std::map<int, Footprint> fp;               // per space
   std::vector<DevBuf<uint8_t>> wflags;        // per staged dataset
   std::vector<DevBuf<int32_t>> wlist;         // per dataset: written footprint positions
+  std::vector<DevBuf<int32_t>> llist;         // per dataset (load == 2): rows to gather
+  std::vector<std::vector<int32_t>> lbeg;     // per dataset, per tile: first entry in llist
   std::vector<std::vector<int32_t>> wbeg;     // per dataset, per tile: first entry in wlist
   StagedParams sp;
   DevBuf<int32_t> region;
@@ -1293,7 +1337,7 @@ static void validate_bindings(const Ctx &ctx, const ChainView &cv, const lt_arg 
         fail(LT_E_EXECUTION, where + ": dataset size does not match its space");
       if (p[1] == 'R' && D.mode != LT_READ)
         fail(LT_E_EXECUTION, where + ": kernel only reads this argument");
-      if (p[1] == 'W' && D.mode != LT_WRITE && D.mode != LT_RW)
+      if ((p[1] == 'W' || p[1] == 'F') && D.mode != LT_WRITE && D.mode != LT_RW)
         fail(LT_E_EXECUTION, where + ": kernel writes this argument (WRITE/RW required)");
       if (p[1] == 'I' && D.mode != LT_INC && D.mode != LT_WRITE)
         fail(LT_E_EXECUTION, where + ": kernel increments this argument (INC required)");
@@ -1789,6 +1833,8 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   }
   H.ds_pos = hp;
   hp += 2 * H.n_ds;
+  H.ld_pos = hp;  // per dataset: (count, position) of its load list (load == 2)
+  hp += 2 * H.n_ds;
   H.prog_pos = hp++;
   H.dep_pos = hp;  // dataflow: (count, position) of the tile's dependency list
   hp += 2;
@@ -1842,6 +1888,9 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   }
   for (int k = 0; k < H.n_ds; ++k)
     if (P.wflags[k].get()) s_wf[k] = (int)secs.size(), sec(P.wlist[k].get(), false);
+  std::vector<int> s_ld(H.n_ds, -1);
+  for (int k = 0; k < H.n_ds; ++k)
+    if (H.ds[k].load == 2) s_ld[k] = (int)secs.size(), sec(P.llist[k].get(), false);
   const int s_dep = P.dataflow ? (int)secs.size() : -1;
   if (P.dataflow) sec(P.nbr.get(), false);
   std::vector<int32_t> hdr(H.hs);
@@ -1903,6 +1952,13 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       const int32_t o = P.wbeg[k][t], n = P.wbeg[k][t + 1] - o;
       hdr[H.ds_pos + 2 * k] = n;
       hdr[H.ds_pos + 2 * k + 1] = put(s_wf[k], o, n, 0);
+    }
+    for (int k = 0; k < H.n_ds; ++k) {
+      hdr[H.ld_pos + 2 * k] = 0;
+      if (s_ld[k] < 0) continue;
+      const int32_t o = P.lbeg[k][t], n = P.lbeg[k][t + 1] - o;
+      hdr[H.ld_pos + 2 * k] = n;
+      hdr[H.ld_pos + 2 * k + 1] = put(s_ld[k], o, n, 0);
     }
     hdr[H.dep_pos] = 0;
     if (s_dep >= 0) {
@@ -2196,6 +2252,76 @@ static void print_plan_stats(const lt_schedule *s, const ExecPlan &P, size_t blo
             (int)P.host_loops[j].nobar);
 }
 
+// Rows that need no gather: a dataset whose first access in the chain is a
+// direct WRITE by a kernel that writes every component ("DF") gets, per tile,
+// the list of its footprint rows that loop does *not* write; only those are
+// gathered (load == 2).  DG: the volume loop writes ru, rs of the tile's
+// cells, so only rows other tiles' cells contribute to are loaded.
+__global__ void k_clear_slots(const int32_t *elements, const int32_t *sigma, int64_t n,
+                              const int32_t *fp_off, const int32_t *slot, uint8_t *flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || slot[i] < 0) return;
+  flag[fp_off[sigma[elements[i]]] + slot[i]] = 0;
+}
+
+static void build_load_lists(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPlan &P,
+                             const std::vector<int> &ds_of, const std::vector<int> &ds_space) {
+  StagedParams &H = P.sp;
+  const int nl = s->n_loops;
+  P.llist.resize(H.n_ds);
+  P.lbeg.resize(H.n_ds);
+  for (int k = 0; k < H.n_ds; ++k) {
+    if (H.ds[k].ro || getenv("LT_LOAD_ALL")) continue;
+    int j0 = -1, d0 = -1, hits = 0;
+    for (int j = 0, q = 0; j < nl && j0 < 0; ++j) {
+      for (size_t d = 0; d < cv.loops[j].desc.size(); ++d)
+        if (ds_of[q + d] == k) {
+          ++hits;
+          if (d0 < 0) d0 = (int)d;
+        }
+      if (hits) j0 = j;
+      q += (int)cv.loops[j].desc.size();
+    }
+    if (j0 < 0 || hits != 1) continue;
+    const lt_desc &D = cv.loops[j0].desc[d0];
+    const char *tok = kSpecs[cv.loops[j0].kernel].sig + 3 * d0;
+    if (D.map >= 0 || D.mode != LT_WRITE || tok[1] != 'F') continue;
+    const Footprint &fp = P.fp.at(ds_space[k]);
+    const int64_t n = fp.n;
+    DevBuf<uint8_t> flag(std::max<int64_t>(n, 1), ctx.stream);
+    LT_CK(cudaMemsetAsync(flag.get(), 1, std::max<int64_t>(n, 1), ctx.stream));
+    const LoopLists &Lj = s->lists[j0];
+    if (Lj.n)
+      k_clear_slots<<<grid_for(Lj.n, 256), 256, 0, ctx.stream>>>(
+          Lj.elements.get(), Lj.sigma.get(), Lj.n, fp.off.get(), P.loops[j0].slots[d0].get(),
+          flag.get());
+    LT_CK_LAUNCH();
+    DevBuf<int32_t> f32(std::max<int64_t>(n, 1), ctx.stream), scan(n + 1, ctx.stream);
+    int64_t cnt = 0;
+    if (n) {
+      k_u8_to_i32<<<grid_for(n, 256), 256, 0, ctx.stream>>>(flag.get(), n, f32.get());
+      LT_CK_LAUNCH();
+      exclusive_sum(ctx, f32.get(), scan.get(), n);
+      cnt = last_plus(ctx, scan.get(), f32.get(), n);
+    }
+    k_set_int<<<1, 1, 0, ctx.stream>>>(scan.get() + n, (int32_t)cnt);
+    LT_CK_LAUNCH();
+    P.llist[k].alloc(std::max<int64_t>(cnt, 1), ctx.stream);
+    if (n) {
+      k_compact_written<<<grid_for(n, 256), 256, 0, ctx.stream>>>(
+          flag.get(), scan.get(), fp.tile.get(), fp.off.get(), n, P.llist[k].get());
+      LT_CK_LAUNCH();
+    }
+    DevBuf<int32_t> lb(s->n_tiles + 1, ctx.stream);
+    k_gather_at<<<grid_for(s->n_tiles + 1, 256), 256, 0, ctx.stream>>>(scan.get(), fp.off.get(),
+                                                                       s->n_tiles + 1, lb.get());
+    LT_CK_LAUNCH();
+    to_host(ctx, lb, s->n_tiles + 1, P.lbeg[k]);
+    LT_CK(cudaStreamSynchronize(ctx.stream));
+    H.ds[k].load = 2;
+  }
+}
+
 static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const ChainView &cv,
                                             const lt_arg *args, int use_local,
                                             bool force_global = false) {
@@ -2420,6 +2546,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       to_host(ctx, wb, s->n_tiles + 1, P.wbeg[k]);
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
+    build_load_lists(ctx, s, cv, P, ds_of, ds_space);
     for (int j = 0; j + 1 < nl; ++j)
       P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j);
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];

@@ -67,7 +67,8 @@ struct StageDS {
   int32_t vpe;
   int32_t stride;          // shared-memory row stride (vpe | 1)
   int32_t sp;              // footprint space index
-  int32_t load;            // 0: every footprint row is written before it is read
+  int32_t load;            // 1: gather every footprint row; 2: only the tile's load list
+                           // (rows its first, full-writing loop does not overwrite)
   int32_t written;         // the tile writes some rows of it (store-back flags present)
   int32_t ro;              // never written by the chain: gathered before dependency waits
   // gather/store-back thread mapping: thread = (row offset < di, component < unit)
