@@ -57,8 +57,14 @@ def golden():
     return golden_schedules()
 
 
-@pytest.fixture(params=["dataflow", "staged", "global"])
+@pytest.fixture(params=["dataflow", "dataflow-wave", "staged", "global"])
 def exec_mode(request, monkeypatch):
-    """Run a GPU executor test with shared-memory staging and with the global path."""
-    monkeypatch.setenv("LT_EXEC", request.param)
+    """Run a GPU executor test with shared-memory staging (dataflow queue in
+    colour-major and in wavefront order, per-colour launches) and with the
+    global path."""
+    mode = request.param
+    if mode == "dataflow-wave":
+        monkeypatch.setenv("LT_ORDER", "wave")
+        mode = "dataflow"
+    monkeypatch.setenv("LT_EXEC", mode)
     return request.param
