@@ -332,6 +332,9 @@ struct StagedParams {
   int32_t ro_packed;                 // rows of read-only datasets follow the program in the blob
   int32_t dep_pos;                   // header position of the dependency list (dataflow)
   int32_t ld_pos;                    // header position of the per-dataset load lists
+  int32_t n_gather, n_store;         // datasets gathered after the dependency wait / stored back
+  int8_t gather_ds[LT_MAX_STAGED];   // their indices (no per-dataset flag tests in the tile)
+  int8_t store_ds[LT_MAX_STAGED];
   int32_t pad;
   const int32_t *blob;
   const int64_t *blob_off;           // per tile: first int of its blob
@@ -617,9 +620,9 @@ template <int FAM, int SB = 1>
 __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base) {
   const int *B = reinterpret_cast<const int *>(smem);
   LT_TSTAMP(t_gather);
-  for (int d = 0; d < P.n_ds; ++d) {
+  for (int q = 0; q < P.n_gather; ++q) {
+    const int d = P.gather_ds[q];
     const StageDS &S = P.ds[d];
-    if (S.ro || !S.load) continue;
     if (S.load == 2)
       gather_rows_listed(S, B, B + B[P.ld_pos + 2 * d + 1], B[P.ld_pos + 2 * d], smem + base[d]);
     else
@@ -734,9 +737,9 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
   }
   LT_TSTAMP(t_wb);
   // store back the rows this tile wrote (coalesced like the gather)
-  for (int d = 0; d < P.n_ds; ++d) {
+  for (int q = 0; q < P.n_store; ++q) {
+    const int d = P.store_ds[q];
     const StageDS &S = P.ds[d];
-    if (!S.written) continue;
     store_rows<SB>(S, B + B[2 * S.sp + 1], B + B[P.ds_pos + 2 * d + 1], B[P.ds_pos + 2 * d],
                smem + base[d]);
   }
@@ -2547,6 +2550,11 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
     build_load_lists(ctx, s, cv, P, ds_of, ds_space);
+    H.n_gather = H.n_store = 0;
+    for (int k = 0; k < H.n_ds; ++k) {
+      if (!H.ds[k].ro && H.ds[k].load) H.gather_ds[H.n_gather++] = (int8_t)k;
+      if (H.ds[k].written) H.store_ds[H.n_store++] = (int8_t)k;
+    }
     for (int j = 0; j + 1 < nl; ++j)
       P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j);
     for (int j = 0; j < nl; ++j) H.loops[j] = P.host_loops[j];
