@@ -332,6 +332,7 @@ struct StagedParams {
   int32_t ro_packed;                 // rows of read-only datasets follow the program in the blob
   int32_t dep_pos;                   // header position of the dependency list (dataflow)
   int32_t ld_pos;                    // header position of the per-dataset load lists
+  int32_t base_pos;                  // header position of the per-dataset row bases
   int32_t n_gather, n_store;         // datasets gathered after the dependency wait / stored back
   int8_t gather_ds[LT_MAX_STAGED];   // their indices (no per-dataset flag tests in the tile)
   int8_t store_ds[LT_MAX_STAGED];
@@ -559,34 +560,24 @@ __device__ __forceinline__ void tile_program_issue(const StagedParams &P, int t,
   bulk_load(smem, P.blob + P.blob_off[t], 4u * (unsigned)P.blob_len[t], bar);
 }
 
-__device__ __forceinline__ void tile_prefetch(const StagedParams &P, int t, double *smem,
-                                              int *base, uint64_t *bar, unsigned phase,
-                                              bool issued = false) {
-  const int tid = threadIdx.x;
+// After the program arrived: the per-dataset row bases are in its header
+// (host-computed, base_pos), so no thread computes them and no barrier is
+// needed -- every thread waits on the program's mbarrier itself.
+__device__ __forceinline__ const int *tile_prefetch(const StagedParams &P, int t, double *smem,
+                                                    uint64_t *bar, unsigned phase,
+                                                    bool issued = false) {
   int *B = reinterpret_cast<int *>(smem);
   LT_TSTAMP(t_blob);
-  if (tid == 0 && !issued) tile_program_issue(P, t, smem, bar);
+  if (threadIdx.x == 0 && !issued) tile_program_issue(P, t, smem, bar);
   mbar_wait(bar, phase);
   LT_TACC(0, t_blob);
-  if (tid == 0) {
-    // rows after the program (a multiple of 4 ints): read-only datasets first
-    // (with ro_packed the blob already holds them there), then the others
-    int acc = B[P.prog_pos] / 2;
-    for (int pass = 1; pass >= 0; --pass)
-      for (int d = 0; d < P.n_ds; ++d) {
-        if (P.ds[d].ro != pass) continue;
-        acc += acc & P.ds[d].vec;  // 16-byte aligned rows for pair copies
-        base[d] = acc;
-        acc += B[2 * P.ds[d].sp] * P.ds[d].stride;
-      }
-    base[P.n_ds] = acc;
-  }
-  __syncthreads();
+  const int *base = B + P.base_pos;
   if (!P.ro_packed) {
     for (int d = 0; d < P.n_ds; ++d)
       if (P.ds[d].ro) gather_rows(P.ds[d], B, smem + base[d]);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  return base;
 }
 
 // Deferred apply of a DG facet loop's chunk: one work item per (unique target,
@@ -617,7 +608,8 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
 // Phase 2: gather the datasets the chain writes, run every loop on shared
 // memory, store back the rows this tile wrote.
 template <int FAM, int SB = 1>
-__device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem, int *base) {
+__device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem,
+                                         const int *base) {
   const int *B = reinterpret_cast<const int *>(smem);
   LT_TSTAMP(t_gather);
   for (int q = 0; q < P.n_gather; ++q) {
@@ -751,11 +743,10 @@ template <int FAM>
 __global__ void __launch_bounds__(LT_SBLOCK) k_staged_tiles(const __grid_constant__ StagedParams P,
                                                             const int32_t *__restrict__ tile_ids) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int base[LT_MAX_STAGED + 1];
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
-  tile_prefetch(P, tile_ids[blockIdx.x], smem, base, &bar, 0);
+  const int *base = tile_prefetch(P, tile_ids[blockIdx.x], smem, &bar, 0);
   run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base);
 }
 
@@ -769,11 +760,10 @@ __global__ void __launch_bounds__(256) k_pack_ro(const __grid_constant__ StagedP
     const int t = order[it];
     const int32_t *B = P.blob + P.blob_off[t];
     double *tile = reinterpret_cast<double *>(const_cast<int32_t *>(B));
-    int acc = B[P.prog_pos] / 2;
     for (int d = 0; d < P.n_ds; ++d) {
       const StageDS &S = P.ds[d];
       if (!S.ro) continue;
-      acc += acc & S.vec;
+      const int acc = B[P.base_pos + d];  // the layout tile_prefetch uses (header)
       const int v = S.vpe, nrow = B[2 * S.sp];
       const int32_t *idx = B + B[2 * S.sp + 1];
       double *rows = tile + acc;
@@ -781,7 +771,6 @@ __global__ void __launch_bounds__(256) k_pack_ro(const __grid_constant__ StagedP
         const int r = w / v, c = w - r * v;
         rows[r * S.stride + c] = __ldg(S.data + ((uint32_t)idx[r] * (uint32_t)v + c));
       }
-      acc += nrow * S.stride;
     }
   }
 }
@@ -820,7 +809,6 @@ template <int FAM, int MINB>
 __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_constant__ StagedParams P,
                                                         const DataflowArgs D) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int base[LT_MAX_STAGED + 1];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int item;
   if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -854,7 +842,7 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
       tile_program_issue(P, t, smem, &bar);
       if (prev >= 0) release(prev);
     }
-    tile_prefetch(P, t, smem, base, &bar, phase, true);  // overlaps the dependency wait
+    const int *base = tile_prefetch(P, t, smem, &bar, phase, true);  // overlaps the dep. wait
     phase ^= 1u;
     LT_TSTAMP(t_wait);
     // the tile's dependency list arrived with its program (one global round
@@ -1836,6 +1824,8 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   }
   H.ds_pos = hp;
   hp += 2 * H.n_ds;
+  H.base_pos = hp;  // per dataset (+ scratch): first double of its rows in smem
+  hp += H.n_ds + 1;
   H.ld_pos = hp;  // per dataset: (count, position) of its load list (load == 2)
   hp += 2 * H.n_ds;
   H.prog_pos = hp++;
@@ -1971,6 +1961,18 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
     }
     cur = (cur + 3) / 4 * 4;  // 16-byte aligned programs
     hdr[H.prog_pos] = (int32_t)cur;
+    {  // row bases: read-only datasets first (packed behind the program), then the others
+      int64_t acc = cur / 2;
+      for (int pass = 1; pass >= 0; --pass)
+        for (int k = 0; k < H.n_ds; ++k) {
+          if (H.ds[k].ro != pass) continue;
+          acc += acc & H.ds[k].vec;  // 16-byte aligned rows for pair copies
+          hdr[H.base_pos + k] = (int32_t)acc;
+          const auto &oh = fps[H.ds[k].sp]->off_host;
+          acc += (int64_t)(oh[t + 1] - oh[t]) * H.ds[k].stride;
+        }
+      hdr[H.base_pos + H.n_ds] = (int32_t)acc;
+    }
     {  // header section
       Section &S = secs[s_hdr];
       S.src_off.push_back((int64_t)hdr_host.size());
