@@ -783,8 +783,8 @@ __global__ void __launch_bounds__(256) k_pack_ro(const __grid_constant__ StagedP
 // by running CTAs, so the schedule cannot deadlock.  Replaces the grid-wide
 // barrier between colour classes by point-to-point tile dependencies.
 struct DataflowArgs {
-  const int32_t *item_t;   // per queue item: tile
-  const int32_t *item_k;   // per queue item: repeat
+  const int64_t *item_tk;  // per queue item: repeat << 32 | tile
+  const int64_t *item_ol;  // per queue item: program ints to bulk-copy << 40 | program offset
   const int32_t *order;    // executable tiles in queue order
   int32_t *done;           // per tile: completed repeats
   int32_t *queue;          // next item
@@ -836,10 +836,14 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
       if (threadIdx.x == 0 && prev >= 0) release(prev);
       return;
     }
-    const int k = D.item_k[it];
-    const int t = D.item_t[it];
+    // the item's tile and its program's offset/length are independent loads
+    // (one global round trip before the program's bulk copy)
+    const long long tk = D.item_tk[it];
+    const int t = (int)(uint32_t)tk, k = (int)(tk >> 32);
     if (threadIdx.x == 0) {
-      tile_program_issue(P, t, smem, &bar);
+      const long long ol = D.item_ol[it];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem reads
+      bulk_load(smem, P.blob + (ol & ((1ll << 40) - 1)), 4u * (unsigned)(ol >> 40), &bar);
       if (prev >= 0) release(prev);
     }
     const int *base = tile_prefetch(P, t, smem, &bar, phase, true);  // overlaps the dep. wait
@@ -1222,7 +1226,12 @@ struct ExecPlan {
   DevBuf<int32_t> order_all, order_core, order_bnd, nbr_off, nbr, done, queue;
   std::vector<int32_t> nbr_off_host, nbr_host;  // dependency lists (queue-order construction)
   std::vector<int32_t> exec_host[3];            // tiles per call kind: all, core, boundary
-  std::map<std::pair<int, int>, std::pair<DevBuf<int32_t>, DevBuf<int32_t>>> items;  // (kind, repeats)
+  struct Items {
+    DevBuf<int64_t> tk, ol;  // per queue item: repeat << 32 | tile; length << 40 | offset
+  };
+  std::map<std::pair<int, int>, Items> items;  // per (call kind, repeats)
+  std::vector<int64_t> blob_off_host;          // per tile: program offset (ints)
+  std::vector<int32_t> blob_len_host, blob_full_host;  // program / program + packed rows
   std::map<std::pair<int, int>, int> items_wave;  // 1: wavefront order chosen
   int n_all = 0, n_core = 0, n_bnd = 0, grid = 0;
   bool wide = false;  // 128-register build (tile programs allow <= 4 CTAs per SM)
@@ -1625,6 +1634,12 @@ static void build_dependencies(Ctx &ctx, lt_schedule *s, ExecPlan &P) {
 //    are as fast with more traffic).
 // Wavefront is used when the staged datasets do not fit in half of L2 (or
 // LT_ORDER=wave); the item list is checked against every dependency either way.
+// read-only rows are packed behind the tile programs when every tile of the
+// call runs more than once (packing costs one pass over those rows)
+static bool pack_for(const ExecPlan &P, int repeats) {
+  return P.sp.ro_packed && repeats >= 2 && !getenv("LT_NO_PACK");
+}
+
 static void build_items(Ctx &ctx, ExecPlan &P, int kind, int repeats, size_t ds_bytes) {
   const std::vector<int32_t> &tiles = P.exec_host[kind];
   const int n = (int)tiles.size();
@@ -1688,12 +1703,22 @@ static void build_items(Ctx &ctx, ExecPlan &P, int kind, int repeats, size_t ds_
   }
   std::fill(pos_of.begin(), pos_of.end(), -1);
   if (!check()) fail(LT_E_EXECUTION, "dataflow queue order violates a tile dependency");
+  const bool packed = pack_for(P, repeats);
+  std::vector<int64_t> tk(ni), ol(ni);
+  for (int64_t q = 0; q < ni; ++q) {
+    const int t = it_t[q];
+    tk[q] = (int64_t)it_k[q] << 32 | (uint32_t)t;
+    const int64_t len = packed ? P.blob_full_host[t] : P.blob_len_host[t];
+    if (P.blob_off_host[t] >= (1ll << 40) || len >= (1ll << 23))
+      fail(LT_E_EXECUTION, "tile program offset/length out of the queue item range");
+    ol[q] = len << 40 | P.blob_off_host[t];
+  }
   auto &dst = P.items[{kind, repeats}];
-  dst.first.alloc(std::max<int64_t>(ni, 1), ctx.stream);
-  dst.second.alloc(std::max<int64_t>(ni, 1), ctx.stream);
+  dst.tk.alloc(std::max<int64_t>(ni, 1), ctx.stream);
+  dst.ol.alloc(std::max<int64_t>(ni, 1), ctx.stream);
   if (ni) {
-    LT_CK(cudaMemcpyAsync(dst.first.get(), it_t.data(), 4 * ni, cudaMemcpyHostToDevice, ctx.stream));
-    LT_CK(cudaMemcpyAsync(dst.second.get(), it_k.data(), 4 * ni, cudaMemcpyHostToDevice, ctx.stream));
+    LT_CK(cudaMemcpyAsync(dst.tk.get(), tk.data(), 8 * ni, cudaMemcpyHostToDevice, ctx.stream));
+    LT_CK(cudaMemcpyAsync(dst.ol.get(), ol.data(), 8 * ni, cudaMemcpyHostToDevice, ctx.stream));
   }
   LT_CK(cudaStreamSynchronize(ctx.stream));
   P.items_wave[{kind, repeats}] = wave ? 1 : 0;
@@ -1997,6 +2022,9 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
     boff[t] = total;
     total += cur;
   }
+  P.blob_off_host = boff;
+  P.blob_len_host = blen;
+  P.blob_full_host = bfull;
   P.blob.alloc(std::max<int64_t>(total, 4), ctx.stream);
   P.blob_off.alloc(nt, ctx.stream);
   P.blob_len.alloc(nt, ctx.stream);
@@ -2701,8 +2729,8 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       const int kind = core && bnd ? 0 : core ? 1 : 2;
       if (!P.items.count({kind, repeats})) build_items(ctx, P, kind, repeats, P.ds_bytes);
       auto &its = P.items.at({kind, repeats});
-      D.item_t = its.first.get();
-      D.item_k = its.second.get();
+      D.item_tk = its.tk.get();
+      D.item_ol = its.ol.get();
       if (info) {
         info->wave_order = P.items_wave.at({kind, repeats});
         info->wide_build = P.wide ? 1 : 0;
@@ -2716,7 +2744,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     // packing costs one pass over the read-only rows: it pays when every tile
     // runs more than once in this call
     StagedParams sp = P.sp;
-    sp.ro_packed = P.sp.ro_packed && repeats >= 2 && !getenv("LT_NO_PACK");
+    sp.ro_packed = pack_for(P, repeats);
     if (sp.ro_packed) sp.blob_len = P.blob_len_full.get();
     if (D.n_items > 0 && sp.ro_packed) {
       k_pack_ro<<<std::min(D.n_exec, 16 * 148), 256, 0, ctx.stream>>>(sp, D.order, D.n_exec);
