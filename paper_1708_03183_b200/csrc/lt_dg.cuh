@@ -136,7 +136,7 @@ __device__ __forceinline__ void dg_iflux(C &c, int q) {
   rb[2 * NQ] = lb * dnb - 2.0 * mub * dvbx * nx;
   rb[3 * NQ] = lb * dnb - 2.0 * mub * dvby * ny;
   rb[4 * NQ] = -mub * (dvbx * ny + dvby * nx);
-  if (q == 0) {
+  if (C::kRecGeo && q == 0) {  // staged records omit |f|/2 and the face (read from fgeo)
     double *r0 = c.rec(0) + 5 * NQ, *r1 = c.rec(1) + 5 * NQ;
     r0[0] = g[2];
     r0[1] = g[3];
@@ -171,7 +171,7 @@ __device__ __forceinline__ void dg_eflux(C &c, int q) {
   r[2 * NQ] = lam * dn + 2.0 * mu * dvx * nx;
   r[3 * NQ] = lam * dn + 2.0 * mu * dvy * ny;
   r[4 * NQ] = mu * (dvx * ny + dvy * nx);
-  if (q == 0) {
+  if (C::kRecGeo && q == 0) {
     c.rec(0)[5 * NQ] = g[2];
     c.rec(0)[5 * NQ + 1] = g[3];
   }
@@ -234,6 +234,21 @@ __device__ __forceinline__ void dg_dispatch(int k, C &c, int lane) {
 }
 
 // deferred apply of one (target row i): acc[f] += lift of each record, in order
+// same with |f|/2 and the face given (staged records carry corrections only)
+template <int FAM>
+__device__ __forceinline__ void dg_lift_acc_g(int k, const double *__restrict__ params, int i,
+                                              const double *rec, double jf, int face,
+                                              double acc[5]) {
+  LT_DG_FAMILY(FAM, k, ({
+                 constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ;
+                 const double *__restrict__ LIFT = params + 3 * NQ * ND;
+                 double o[5];
+                 dg_lift_row<ND, NQ>(LIFT, face, i, jf, rec, o);
+#pragma unroll
+                 for (int f = 0; f < 5; ++f) acc[f] += o[f];
+               }));
+}
+
 template <int FAM>
 __device__ __forceinline__ void dg_lift_acc(int k, const double *__restrict__ params, int i,
                                             const double *rec, double acc[5]) {
@@ -256,6 +271,9 @@ inline int dg_lanes(int k) {
 // doubles of one per-side correction record: 5 NQ corrections, jf, face
 // (record stride rounded up to odd: conflict-free 64-bit shared-memory reads)
 inline int dg_corr_size(int k) { return (5 * (k / 5 + 2) + 2) | 1; }
+// staged executors: corrections only (|f|/2 and the face come from the facet's
+// geometry row), stride rounded up to odd
+inline int dg_corr_size_staged(int k) { return (5 * (k / 5 + 2)) | 1; }
 inline bool dg_is_flux(int k) { return k % 5 == 1 || k % 5 == 2; }
 
 inline int64_t dg_param_count(int k) {

@@ -55,6 +55,7 @@ static int sig_count(const char *sig) {
 
 // ---- access contexts ------------------------------------------------------------
 struct TileCtx {
+  static constexpr bool kRecGeo = true;  // records carry |f|/2 and the face
   const DLoop &L;
   int e, gpos, lpos;
   double *smem;
@@ -79,6 +80,7 @@ struct TileCtx {
 };
 
 struct FlatCtx {  // untiled: element ids, global scratch
+  static constexpr bool kRecGeo = true;
   const DLoop &L;
   int e;
   __device__ int vpe(int d) const { return L.a[d].vpe; }
@@ -103,6 +105,7 @@ struct FlatCtx {  // untiled: element ids, global scratch
 // staged: every dataset row the tile touches lives in shared memory; slots are
 // footprint-local row indices produced by the plan
 struct StagedCtx {
+  static constexpr bool kRecGeo = false;  // |f|/2 and face read from the facet geometry row
   const DLoop &L;
   int e, pos, lpos;  // pos: position in the tile's list
   double *smem;
@@ -588,17 +591,30 @@ template <int FAM>
 __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off, const int *utgt,
                                                const int *ut_off, const int *slots, int c,
                                                const double *scratch, double *smem,
-                                               const int *base) {
+                                               const int *base, const int *fslot) {
   if (FAM == 0) return;
-  const DArg &Au = L.a[4], &As = L.a[5];
+  const DArg &Au = L.a[4], &As = L.a[5], &Ag = L.a[0];
   const int nd = Au.vpe >> 1;
+  const bool two = Au.arity == 2;
   double *ru = smem + base[Au.ds], *rs = smem + base[As.ds];
+  const double *geo = smem + base[Ag.ds];
   const int u0 = gc_off[c], nu = gc_off[c + 1] - u0;
   int q = lt_div(threadIdx.x, nd, L.row_magic), i = threadIdx.x - q * nd;
   while (q < nu) {
     const int u = u0 + q;
-    lift_apply_item<FAM>(L, ru + utgt[u] * Au.sstride + i, rs + utgt[u] * As.sstride + i, nd, i,
-                         scratch, slots, ut_off[u], ut_off[u + 1]);
+    double *du = ru + utgt[u] * Au.sstride + i, *ds = rs + utgt[u] * As.sstride + i;
+    double acc[5] = {du[0], du[nd], ds[0], ds[nd], ds[2 * nd]};
+    for (int s = ut_off[u], s1 = ut_off[u + 1]; s < s1; ++s) {
+      const int sl = slots[s], lp = two ? sl >> 1 : sl, k = two ? sl & 1 : 0;
+      const double *g = geo + fslot[lp] * Ag.sstride;  // facet geometry [nx ny |f|/2 fa fb]
+      dg_lift_acc_g<FAM>(L.kernel - K_DG_FIRST, L.params, i, scratch + (size_t)sl * L.rec, g[2],
+                         (int)g[3 + k], acc);
+    }
+    du[0] = acc[0];
+    du[nd] = acc[1];
+    ds[0] = acc[2];
+    ds[nd] = acc[3];
+    ds[2 * nd] = acc[4];
     q += L.row_dq;
     i += L.row_dr;
     if (i >= nd) { i -= nd; ++q; }
@@ -655,7 +671,9 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
         }
         __syncthreads();
         LT_TACC(40 + (j < 23 ? j : 23), t_rec);
-        apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base);
+        // fslot: the chunk's facet-geometry slots (descriptor 0, direct)
+        apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base,
+                            B + LH[2] + c0);
         __syncthreads();
       }
       LT_TACC(8 + (j < 24 ? j : 23), t_loop);
@@ -1219,6 +1237,7 @@ struct ExecPlan {
   DevBuf<int64_t> blob_off;
   size_t data_max = 0;  // largest per-tile dataset rows (bytes)
   size_t ds_bytes = 0;  // total bytes of the staged datasets (queue-order choice)
+  size_t scratch_bytes = 0;  // contribution/record scratch per CTA
   std::vector<size_t> tile_rows;   // per tile: dataset-row bytes (diagnostics)
   std::vector<int32_t> tile_blob;  // per tile: tile-program ints (diagnostics)
   // dataflow
@@ -1237,11 +1256,11 @@ struct ExecPlan {
   bool wide = false;  // 128-register build (tile programs allow <= 4 CTAs per SM)
 };
 
-static int choose_chunk(int scratch_per_pos, size_t smem_budget, int block) {
+static int choose_chunk(int scratch_per_pos, size_t smem_budget, int block, bool round = true) {
   if (scratch_per_pos == 0) return block;
   int ch = (int)(smem_budget / (sizeof(double) * (size_t)scratch_per_pos));
   ch = std::min(ch, block);
-  if (ch >= 32) ch -= ch % 32;
+  if (round && ch >= 32) ch -= ch % 32;
   if (ch < 1) fail(LT_E_EXECUTION, "loop contributions exceed shared memory");
   return ch;
 }
@@ -2355,9 +2374,12 @@ static void build_load_lists(Ctx &ctx, lt_schedule *s, const ChainView &cv, Exec
   }
 }
 
+// scratch_override > 0: record budget for the deferred (DG facet) loops, chunks
+// not rounded to warps (second planning pass, see plan_with_occupancy)
 static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const ChainView &cv,
                                             const lt_arg *args, int use_local,
-                                            bool force_global = false) {
+                                            bool force_global = false,
+                                            size_t scratch_override = 0) {
   auto plan = std::make_shared<ExecPlan>();
   ExecPlan &P = *plan;
   const int nl = s->n_loops;
@@ -2377,7 +2399,9 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     P.dataflow = P.staged && pref != 1;
   }
   const int block = P.staged ? LT_SBLOCK : LT_BLOCK;
-  const size_t budget = P.staged ? std::min<size_t>(scratch_budget(), kSmemMax - regions_max)
+  const size_t budget = P.staged ? std::min<size_t>(scratch_override ? scratch_override
+                                                                     : scratch_budget(),
+                                                    kSmemMax - regions_max)
                                  : kSmemBudget;
   size_t scratch_max = 0;
   int a = 0;
@@ -2386,6 +2410,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     LoopPlan &LP = P.loops[j];
     DLoop &D = P.host_loops[j];
     fill_dloop(D, cv, j, args + a, ctx, use_local);
+    if (P.staged && D.deferred) D.rec = dg_corr_size_staged(L.kernel - K_DG_FIRST);
     int spp = 0;
     for (int d = 0; d < D.n_desc; ++d) {
       if (L.desc[d].map < 0 || L.desc[d].mode == LT_READ) continue;
@@ -2398,7 +2423,9 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     LP.deferred = D.deferred;
     if (D.deferred) spp = D.a[4].arity * D.rec;
     LP.scratch_per_pos = spp;
-    LP.chunk = choose_chunk(spp, budget, block);
+    // staged deferred loops: the whole budget (a chunk is one records phase
+    // and one apply phase; fewer chunks, fewer phases per tile)
+    LP.chunk = choose_chunk(spp, budget, block, !(P.staged && D.deferred && scratch_override));
     if (spp) {  // no larger than the longest tile list of the loop (scratch is per CTA)
       std::vector<int32_t> off(s->n_tiles + 1);
       LT_CK(cudaMemcpyAsync(off.data(), s->lists[j].offsets.get(), 4 * (s->n_tiles + 1),
@@ -2600,6 +2627,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       return nullptr;
     }
     P.smem_bytes = blob_max + P.data_max + scratch_max;
+    P.scratch_bytes = scratch_max;
     if (const char *pad = getenv("LT_SMEM_PAD_KB"))  // diagnostics: force lower occupancy
       P.smem_bytes = std::min(kSmemMax, P.smem_bytes + 1024 * (size_t)atoi(pad));
     if (getenv("LT_DEBUG_PLAN")) print_plan_stats(s, P, blob_max, scratch_max);
@@ -2664,6 +2692,59 @@ static DataflowFn dataflow_fn(int fam, bool wide = false) {
   }
 }
 
+// CTAs per SM of the dataflow build that would run a plan with this much
+// shared memory (the 128-register build when <= 4 fit, as in execute_tiled)
+static int dataflow_occupancy(int fam, size_t smem) {
+  auto occ = [&](const void *fn) {
+    int per_sm = 0;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+      cudaGetLastError();  // beyond the kernel's limit (static shared memory included)
+      return 0;
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LT_SBLOCK, smem) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return per_sm;
+  };
+  int per_sm = occ((const void *)dataflow_fn(fam, false));
+  if (per_sm <= LT_WIDE_MINB && fam >= 1 && fam <= 4 && !getenv("LT_NARROW"))
+    per_sm = occ((const void *)dataflow_fn(fam, true));
+  return per_sm;
+}
+
+// Two planning passes for DG chains on the dataflow executor: the first with
+// the default record budget fixes the CTAs per SM the tile programs allow;
+// the second gives the facet loops' correction records all shared memory that
+// keeps that occupancy (bigger chunks: fewer records + ordered-apply phases
+// per tile).  Config 3: 14.66 -> ~14.1 ms; config 2 keeps 7 CTAs/SM.
+static std::shared_ptr<ExecPlan> plan_with_occupancy(Ctx &ctx, lt_schedule *s,
+                                                     const ChainView &cv, const lt_arg *args,
+                                                     int use_local) {
+  auto plan = build_plan(ctx, s, cv, args, use_local);
+  if (!plan || !plan->dataflow || getenv("LT_SCRATCH_KB")) return plan;
+  bool deferred = false;
+  for (const LoopPlan &LP : plan->loops) deferred |= LP.deferred;
+  if (!deferred) return plan;
+  const int fam = chain_family(cv);
+  const int occ = dataflow_occupancy(fam, plan->smem_bytes);
+  const size_t fixed = plan->smem_bytes - plan->scratch_bytes;
+  size_t best = plan->scratch_bytes;
+  for (size_t sc = kSmemMax - 1024 - fixed; sc > plan->scratch_bytes + 512; sc -= 256)
+    if (dataflow_occupancy(fam, fixed + sc) >= occ) {
+      best = sc;
+      break;
+    }
+  if (best < plan->scratch_bytes + 1024) return plan;
+  // the blob grows slightly with longer chunks' plans: leave 1 KB of slack
+  auto p2 = build_plan(ctx, s, cv, args, use_local, false, best - 1024);
+  if (p2 && p2->dataflow && dataflow_occupancy(fam, p2->smem_bytes) >= occ) return p2;
+  return plan;
+}
+
 static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_arg *args,
                           int phases, int use_local, int repeats, lt_exec_info *info) {
   if ((int)cv.loops.size() != s->n_loops)
@@ -2677,7 +2758,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   validate_bindings(ctx, cv, args);
   const std::string key = plan_key(cv, args, use_local) + std::to_string(exec_preference());
   if (!s->plan || s->plan->key != key) {
-    s->plan = build_plan(ctx, s, cv, args, use_local);
+    s->plan = plan_with_occupancy(ctx, s, cv, args, use_local);
     if (!s->plan) {  // tile programs do not fit shared memory
       if (exec_preference() > 0)
         fail(LT_E_EXECUTION, "LT_EXEC=staged/dataflow: " + g_last_fit);
