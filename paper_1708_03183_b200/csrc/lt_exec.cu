@@ -2692,6 +2692,12 @@ static DataflowFn dataflow_fn(int fam, bool wide = false) {
   }
 }
 
+#ifndef LT_PASS2_MIN
+#define LT_PASS2_MIN 1024   // re-plan only for at least this much more record scratch
+#endif
+#ifndef LT_PASS2_SLACK
+#define LT_PASS2_SLACK 1024  // left for the longer chunks' apply plans in the tile programs
+#endif
 // CTAs per SM of the dataflow build that would run a plan with this much
 // shared memory (the 128-register build when <= 4 fit, as in execute_tiled)
 static int dataflow_occupancy(int fam, size_t smem) {
@@ -2738,9 +2744,9 @@ static std::shared_ptr<ExecPlan> plan_with_occupancy(Ctx &ctx, lt_schedule *s,
       best = sc;
       break;
     }
-  if (best < plan->scratch_bytes + 1024) return plan;
+  if (best < plan->scratch_bytes + LT_PASS2_MIN) return plan;
   // the blob grows slightly with longer chunks' plans: leave 1 KB of slack
-  auto p2 = build_plan(ctx, s, cv, args, use_local, false, best - 1024);
+  auto p2 = build_plan(ctx, s, cv, args, use_local, false, best - LT_PASS2_SLACK);
   if (p2 && p2->dataflow && dataflow_occupancy(fam, p2->smem_bytes) >= occ) return p2;
   return plan;
 }
