@@ -1233,7 +1233,6 @@ struct ExecPlan {
   std::vector<int32_t> rank;  // execution order key: colour refined by write-conflict sub-colour
   int max_subcolor = 0;
   DevBuf<int32_t> blob, blob_len;
-  DevBuf<int32_t> blob_len_full;  // program + packed read-only rows (ints), when packable
   DevBuf<int64_t> blob_off;
   size_t data_max = 0;  // largest per-tile dataset rows (bytes)
   size_t ds_bytes = 0;  // total bytes of the staged datasets (queue-order choice)
@@ -2049,11 +2048,6 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   P.blob_len.alloc(nt, ctx.stream);
   LT_CK(cudaMemcpyAsync(P.blob_off.get(), boff.data(), 8 * nt, cudaMemcpyHostToDevice, ctx.stream));
   LT_CK(cudaMemcpyAsync(P.blob_len.get(), blen.data(), 4 * nt, cudaMemcpyHostToDevice, ctx.stream));
-  if (H.ro_packed) {
-    P.blob_len_full.alloc(nt, ctx.stream);
-    LT_CK(cudaMemcpyAsync(P.blob_len_full.get(), bfull.data(), 4 * nt, cudaMemcpyHostToDevice,
-                          ctx.stream));
-  }
   DevBuf<int32_t> hdr_dev(std::max<int64_t>((int64_t)hdr_host.size(), 1), ctx.stream);
   if (!hdr_host.empty())
     LT_CK(cudaMemcpyAsync(hdr_dev.get(), hdr_host.data(), 4 * hdr_host.size(),
@@ -2832,7 +2826,6 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     // runs more than once in this call
     StagedParams sp = P.sp;
     sp.ro_packed = pack_for(P, repeats);
-    if (sp.ro_packed) sp.blob_len = P.blob_len_full.get();
     if (D.n_items > 0 && sp.ro_packed) {
       k_pack_ro<<<std::min(D.n_exec, 16 * 148), 256, 0, ctx.stream>>>(sp, D.order, D.n_exec);
       LT_CK_LAUNCH();
