@@ -819,10 +819,9 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
   return v;
 }
 
-// MINB: CTAs per SM the register budget is sized for (7: 72 registers, the
-// occupancy small tile programs reach; 4: 128 registers for footprints whose
-// shared memory allows at most 4 CTAs per SM -- those tiles are long enough
-// that batched store-back and unspilled bodies pay)
+// MINB: CTAs per SM the register budget is sized for (6: 80 registers -- at P1
+// this beats 72 registers at 7 CTAs/SM, which spill, by 1.5 %; 4: 128
+// registers for footprints whose shared memory allows at most 4 CTAs per SM)
 template <int FAM, int MINB>
 __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_constant__ StagedParams P,
                                                         const DataflowArgs D) {
@@ -2666,7 +2665,7 @@ typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
 #define LT_WIDE_MINB 4  // CTAs per SM of the wide (128-register at 128 threads) build
 #endif
 #ifndef LT_NARROW_MINB
-#define LT_NARROW_MINB 7  // CTAs per SM of the narrow (72-register at 128 threads) build
+#define LT_NARROW_MINB 6  // CTAs per SM of the narrow (80-register at 128 threads) build
 #endif
 static DataflowFn dataflow_fn(int fam, bool wide = false) {
   if (wide) switch (fam) {
@@ -2720,7 +2719,7 @@ static int dataflow_occupancy(int fam, size_t smem) {
 // the default record budget fixes the CTAs per SM the tile programs allow;
 // the second gives the facet loops' correction records all shared memory that
 // keeps that occupancy (bigger chunks: fewer records + ordered-apply phases
-// per tile).  Config 3: 14.66 -> ~14.1 ms; config 2 keeps 7 CTAs/SM.
+// per tile).  Config 3: 14.66 -> ~14.1 ms; config 2: one chunk per tile.
 static std::shared_ptr<ExecPlan> plan_with_occupancy(Ctx &ctx, lt_schedule *s,
                                                      const ChainView &cv, const lt_arg *args,
                                                      int use_local) {
@@ -2769,7 +2768,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   ExecPlan &P = *s->plan;
   const int fam = chain_family(cv);
   if (P.dataflow && P.grid == 0) {
-    // register budget: the 72-register build reaches 7 CTAs per SM; when the
+    // register budget: the 80-register build reaches 6 CTAs per SM; when the
     // tile programs' shared memory allows at most 4, the 128-register build
     // costs no occupancy and spills nothing
     int per_sm = 0, sms = 0;
@@ -2790,7 +2789,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     P.grid = std::max(1, per_sm) * sms;
     if (getenv("LT_DEBUG_PLAN"))
       fprintf(stderr, "[lt plan] dataflow %s build, %d CTAs/SM, grid %d\n",
-              P.wide ? "128-register" : "72-register", per_sm, P.grid);
+              P.wide ? "wide" : "narrow", per_sm, P.grid);
   }
   const void *fn = P.dataflow  ? (const void *)dataflow_fn(fam, P.wide)
                    : P.staged ? (const void *)staged_fn(fam)
