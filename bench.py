@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (nx, ny, p, steps_per_chain, chains_per_job, material, ts, renumber)
-    2: dict(nx=256, ny=256, p=1, T=1, chains=10, material="homogeneous", ts=28,
+    2: dict(nx=256, ny=256, p=1, T=1, chains=10, material="homogeneous", ts=32,
             workload="elastic DG P1 256x256 (131072 cells), 1 timestep/chain, 10 timesteps"),
     3: dict(nx=2048, ny=2048, p=2, T=2, chains=1, material=("uniform", 2), ts=24,
             workload="elastic DG P2 2048x2048 (8.4M cells), 2 timesteps/chain, heterogeneous"),
