@@ -820,8 +820,9 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
 }
 
 // MINB: CTAs per SM the register budget is sized for (6: 80 registers -- at P1
-// this beats 72 registers at 7 CTAs/SM, which spill, by 1.5 %; 4: 128
-// registers for footprints whose shared memory allows at most 4 CTAs per SM)
+// this beats 72 registers at 7 CTAs/SM, which spill, by 1.5 %; 3: 168
+// registers for footprints whose shared memory allows at most 3 CTAs per SM --
+// config 3, 0.7 % faster than 128 registers)
 template <int FAM, int MINB>
 __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_constant__ StagedParams P,
                                                         const DataflowArgs D) {
@@ -1251,7 +1252,7 @@ struct ExecPlan {
   std::vector<int32_t> blob_len_host, blob_full_host;  // program / program + packed rows
   std::map<std::pair<int, int>, int> items_wave;  // 1: wavefront order chosen
   int n_all = 0, n_core = 0, n_bnd = 0, grid = 0;
-  bool wide = false;  // 128-register build (tile programs allow <= 4 CTAs per SM)
+  bool wide = false;  // wide build (tile programs allow <= LT_WIDE_MINB CTAs per SM)
 };
 
 static int choose_chunk(int scratch_per_pos, size_t smem_budget, int block, bool round = true) {
@@ -2662,7 +2663,7 @@ static StagedFn staged_fn(int fam) {
 
 typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
 #ifndef LT_WIDE_MINB
-#define LT_WIDE_MINB 4  // CTAs per SM of the wide (128-register at 128 threads) build
+#define LT_WIDE_MINB 3  // CTAs per SM of the wide (168-register at 128 threads) build
 #endif
 #ifndef LT_NARROW_MINB
 #define LT_NARROW_MINB 6  // CTAs per SM of the narrow (80-register at 128 threads) build
@@ -2692,7 +2693,7 @@ static DataflowFn dataflow_fn(int fam, bool wide = false) {
 #define LT_PASS2_SLACK 1024  // left for the longer chunks' apply plans in the tile programs
 #endif
 // CTAs per SM of the dataflow build that would run a plan with this much
-// shared memory (the 128-register build when <= 4 fit, as in execute_tiled)
+// shared memory (the wide build when <= LT_WIDE_MINB fit, as in execute_tiled)
 static int dataflow_occupancy(int fam, size_t smem) {
   auto occ = [&](const void *fn) {
     int per_sm = 0;
@@ -2769,7 +2770,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   const int fam = chain_family(cv);
   if (P.dataflow && P.grid == 0) {
     // register budget: the 80-register build reaches 6 CTAs per SM; when the
-    // tile programs' shared memory allows at most 4, the 128-register build
+    // tile programs' shared memory allows at most 3, the 168-register build
     // costs no occupancy and spills nothing
     int per_sm = 0, sms = 0;
     const void *narrow = (const void *)dataflow_fn(fam, false);
