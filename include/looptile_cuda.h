@@ -141,7 +141,7 @@ typedef struct {
     int32_t staged;      /* 0: global-memory tiles, 1: staged per colour, 2: staged dataflow */
     int32_t smem_bytes;  /* dynamic shared memory per CTA */
     int32_t wave_order;  /* dataflow queue: 1 wavefront (L2-local) order, 0 colour-major */
-    int32_t wide_build;  /* dataflow: 1 when the 128-register build ran (<= 4 CTAs/SM) */
+    int32_t wide_build;  /* dataflow: 1 when the 168-register build ran (<= 3 CTAs/SM) */
 } lt_exec_info;
 
 /* ---- library / context ---------------------------------------------------- */
@@ -240,9 +240,28 @@ int lt_execute(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain, const lt_arg 
  * overlaps consecutive repeats tile by tile */
 int lt_execute_repeat(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain, const lt_arg *args,
                       int32_t repeats, int32_t use_local_maps, lt_exec_info *info);
+/* Build the execution plan (tile programs, dependency graph, queue) that a
+ * later lt_execute / lt_execute_repeat with the same arguments uses, without
+ * launching anything or touching the datasets.  No reference counterpart: the
+ * reference executor has no plan (executor.py:185-245); this splits its
+ * one-time validation from the steady-state call so time-stepping drivers and
+ * CUDA-graph capture never run the chain just to build the plan. */
+int lt_prepare(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain, const lt_arg *args,
+               int32_t phases, int32_t repeats, int32_t use_local_maps, lt_exec_info *info);
 /* execute_untiled: loops in order, elements ascending (executor.py:163-169) */
 int lt_execute_untiled(lt_ctx *ctx, const lt_chain *chain, const lt_arg *args,
                        lt_exec_info *info);
+
+/* Legality of a schedule (reference pkg/tests/legality.py:15-151, the
+ * brute-force dependence oracle the reference's property tests use): counts
+ * the distinct cross-loop dependence pairs (flow/anti/output through a shared
+ * (space, element), not both direct) whose later element runs in a different
+ * tile of a colour not above the earlier one's, and the reduction pairs
+ * (same loop, mapped increments of one key) split over distinct tiles of equal
+ * colour.  Runs on the GPU at any size; overflow = 1 when more than 2^20
+ * violations were found (counts are then lower bounds). */
+int lt_check_legality(lt_ctx *ctx, const lt_schedule *s, const lt_chain *chain,
+                      int64_t *n_pairs, int64_t *n_reductions, int32_t *overflow);
 
 /* ---- halo exchange packing (distsim.py:48-81) ------------------------------ */
 /* out[i*vpe + c] = values[rows[i]*vpe + c] for i < n_rows (device arrays) */

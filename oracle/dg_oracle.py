@@ -126,10 +126,12 @@ class RefProblem:
 
 
 def build_problem_reference(L, dims, p: int, steps: int = 1, seed: int = 1,
-                            material="homogeneous") -> RefProblem:
-    """Declare the elastic chain on the reference API with numpy bodies."""
+                            material="homogeneous", sigma: float | None = None) -> RefProblem:
+    """Declare the elastic chain on the reference API with numpy bodies.
+
+    ``sigma`` defaults to max(dims)/8 (small fixtures); BASELINE config 2 uses 8."""
     st = elastic_setup(dims[0], dims[1], p, steps, material=material, noise_seed=seed,
-                       sigma=max(dims) / 8.0)
+                       sigma=max(dims) / 8.0 if sigma is None else sigma)
     sp = {n: L.IterationSpace(n, s.core_size, s.boundary_size, s.nonexec_size)
           for n, s in st.spaces.items()}
     mp = {n: L.MeshMap(n, sp[m.source.name], sp[m.target.name], m.arity, m.values)

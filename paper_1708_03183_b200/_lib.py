@@ -112,6 +112,10 @@ SIGNATURES = {
                              C.c_int32, C.POINTER(LtExecInfo)]),
     "lt_execute_repeat": (C.c_int, [_P, _P, C.POINTER(LtChain), C.POINTER(LtArg), C.c_int32,
                                     C.c_int32, C.POINTER(LtExecInfo)]),
+    "lt_prepare": (C.c_int, [_P, _P, C.POINTER(LtChain), C.POINTER(LtArg), C.c_int32,
+                             C.c_int32, C.c_int32, C.POINTER(LtExecInfo)]),
+    "lt_check_legality": (C.c_int, [_P, _P, C.POINTER(LtChain), _I64P, _I64P,
+                                    C.POINTER(C.c_int32)]),
     "lt_execute_untiled": (C.c_int, [_P, C.POINTER(LtChain), C.POINTER(LtArg),
                                      C.POINTER(LtExecInfo)]),
     "lt_halo_pack": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int64, _P]),
@@ -514,6 +518,26 @@ def execute_repeat(sched: ScheduleHandle, chain_desc: ChainDesc, args, repeats: 
     check(load().lt_execute_repeat(sched.ctx.bind_stream(), sched.handle, chain_desc.ref, args,
                                    int(repeats), int(bool(use_local_maps)), C.byref(info)))
     return info
+
+
+def prepare(sched: ScheduleHandle, chain_desc: ChainDesc, args, phases: int, repeats: int,
+            use_local_maps: bool) -> LtExecInfo:
+    """Build the execution plan of a later execute/execute_repeat; launches nothing."""
+    info = LtExecInfo()
+    check(load().lt_prepare(sched.ctx.bind_stream(), sched.handle, chain_desc.ref, args,
+                            int(phases), int(repeats), int(bool(use_local_maps)),
+                            C.byref(info)))
+    return info
+
+
+def check_legality(sched: ScheduleHandle, chain_desc: ChainDesc) -> dict:
+    pairs, red, ovf = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+    check(load().lt_check_legality(sched.ctx.bind_stream(), sched.handle, chain_desc.ref,
+                                   C.byref(pairs), C.byref(red), C.byref(ovf)))
+    out = {"pairs": pairs.value, "reductions": red.value}
+    if ovf.value:
+        out["overflow"] = True
+    return out
 
 
 def execute_untiled(chain_desc: ChainDesc, args) -> LtExecInfo:

@@ -128,12 +128,20 @@ extern "C" int lt_ctx_set_kernel_params(lt_ctx *ctx, int32_t kernel_id, const do
   LT_API_BEGIN
   if (!ctx) fail(LT_E_VALUE, "null context");
   if (kernel_id < 0 || kernel_id >= lt_kernel_count()) fail(LT_E_EXECUTION, "unknown kernel id");
-  DevBuf<double> buf(std::max<int64_t>(n, 1), ctx->stream);
+  // Update in place when the block fits: cached execution plans and captured
+  // CUDA graphs hold the device pointer, so they see the new values.  A block
+  // that must grow is reallocated and the generation bump invalidates every
+  // cached plan (graphs captured before that must be re-captured).
+  auto it = ctx->params.find(kernel_id);
+  if (it == ctx->params.end() || it->second.n < std::max<int64_t>(n, 1)) {
+    DevBuf<double> buf(std::max<int64_t>(n, 1), ctx->stream);
+    ctx->params[kernel_id] = std::move(buf);
+    ++ctx->params_gen;
+  }
   if (n > 0)
-    LT_CK(cudaMemcpyAsync(buf.get(), host, sizeof(double) * n, cudaMemcpyHostToDevice,
-                          ctx->stream));
+    LT_CK(cudaMemcpyAsync(ctx->params[kernel_id].get(), host, sizeof(double) * n,
+                          cudaMemcpyHostToDevice, ctx->stream));
   LT_CK(cudaStreamSynchronize(ctx->stream));
-  ctx->params[kernel_id] = std::move(buf);
   LT_API_END
 }
 

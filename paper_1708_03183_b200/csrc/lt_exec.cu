@@ -1242,6 +1242,7 @@ struct ExecPlan {
   // dataflow
   bool dataflow = false;
   DevBuf<int32_t> order_all, order_core, order_bnd, nbr_off, nbr, done, queue;
+  int last_call = -1;  // dataflow: 0 both phases, 1 core only, 2 boundary only
   std::vector<int32_t> nbr_off_host, nbr_host;  // dependency lists (queue-order construction)
   std::vector<int32_t> exec_host[3];            // tiles per call kind: all, core, boundary
   struct Items {
@@ -1432,8 +1433,9 @@ static void fill_dloop(DLoop &D, const ChainView &cv, int j, const lt_arg *args,
   }
 }
 
-static std::string plan_key(const ChainView &cv, const lt_arg *args, int use_local) {
-  std::string k = std::to_string(use_local) + "|";
+static std::string plan_key(const Ctx &ctx, const ChainView &cv, const lt_arg *args,
+                            int use_local) {
+  std::string k = std::to_string(use_local) + "|" + std::to_string(ctx.params_gen) + "|";
   int a = 0;
   for (const LoopDesc &L : cv.loops) {
     k += std::to_string(L.kernel) + ":";
@@ -1457,6 +1459,11 @@ static size_t scratch_budget() {
 }
 static std::string g_last_fit;
 static const size_t kSmemMax = 227 * 1024;
+
+__global__ void k_zero_at(int32_t *v, const int32_t *idx, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[idx[i]] = 0;
+}
 
 // ---- tile dependency graph of the dataflow executor ---------------------------------
 // Two tiles depend on each other iff their footprints share an element of some
@@ -1672,15 +1679,33 @@ static void build_items(Ctx &ctx, ExecPlan &P, int kind, int repeats, size_t ds_
     for (int i = 0; i < n; ++i, ++q) it_t[q] = tiles[i], it_k[q] = k;
   const int tmax = n ? *std::max_element(tiles.begin(), tiles.end()) + 1 : 1;
   std::vector<int32_t> pos_of((size_t)repeats * tmax, -1);
+  // a same-repeat dependency outside this call's queue is only satisfied by an
+  // earlier call when this is the boundary-only call and the dependency is a
+  // core tile (its core-only call ran first: the host checks that order);
+  // anything else would spin forever on the device
+  std::vector<char> is_core;
+  if (kind == 2) {
+    is_core.assign(P.rank.size(), 0);
+    for (int t : P.exec_host[1]) is_core[t] = 1;
+  }
+  auto outside_ok = [&](int u) { return kind == 2 && u < (int)is_core.size() && is_core[u]; };
   auto check = [&]() {
     for (int64_t q = 0; q < ni; ++q) pos_of[(size_t)it_k[q] * tmax + it_t[q]] = (int32_t)q;
     for (int64_t q = 0; q < ni; ++q) {
       const int t = it_t[q], k = it_k[q];
       for (int e = P.nbr_off_host[t]; e < P.nbr_off_host[t + 1]; ++e) {
         const int u = P.nbr_host[e] >> 1, rep = k + (P.nbr_host[e] & 1) - 1;
-        if (rep < 0 || u >= tmax) continue;
-        const int32_t pu = pos_of[(size_t)rep * tmax + u];
-        if (pu >= 0 && pu >= q) return false;
+        if (rep < 0) continue;
+        const int32_t pu = u < tmax ? pos_of[(size_t)rep * tmax + u] : -1;
+        if (pu < 0) {
+          if ((P.nbr_host[e] & 1) && !outside_ok(u))
+            fail(LT_E_EXECUTION, "dataflow: tile " + std::to_string(t) + " depends on tile " +
+                                     std::to_string(u) + " of a lower colour that this call "
+                                     "does not execute (boundary colours must exceed core "
+                                     "colours)");
+          continue;
+        }
+        if (pu >= q) return false;
       }
     }
     return true;
@@ -2745,8 +2770,11 @@ static std::shared_ptr<ExecPlan> plan_with_occupancy(Ctx &ctx, lt_schedule *s,
   return plan;
 }
 
+// dry: build the plan and queue items, report what a call would launch, and
+// launch nothing (lt_prepare: plan building without touching the datasets)
 static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_arg *args,
-                          int phases, int use_local, int repeats, lt_exec_info *info) {
+                          int phases, int use_local, int repeats, lt_exec_info *info,
+                          bool dry = false) {
   if ((int)cv.loops.size() != s->n_loops)
     fail(LT_E_STALE_SCHEDULE, "schedule loop count differs from chain");
   for (int j = 0; j < s->n_loops; ++j)
@@ -2756,7 +2784,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
   if (repeats > 1 && phases != (LT_PHASE_CORE | LT_PHASE_BOUNDARY))
     fail(LT_E_VALUE, "repeated execution needs both phases (no halo exchange in between)");
   validate_bindings(ctx, cv, args);
-  const std::string key = plan_key(cv, args, use_local) + std::to_string(exec_preference());
+  const std::string key = plan_key(ctx, cv, args, use_local) + std::to_string(exec_preference());
   if (!s->plan || s->plan->key != key) {
     s->plan = plan_with_occupancy(ctx, s, cv, args, use_local);
     if (!s->plan) {  // tile programs do not fit shared memory
@@ -2819,13 +2847,28 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     }
     D.done = P.done.get();
     D.queue = P.queue.get();
-    if (core)  // a boundary-only call continues the counters of its core call
+    // a boundary-only call continues the counters of the core-only call that
+    // must directly precede it (its core dependencies are complete); its own
+    // tiles' counters restart at zero so overlapping boundary tiles still wait
+    if (!core && !dry && P.last_call != 1)
+      fail(LT_E_EXECUTION, "dataflow: a boundary-only execution must directly follow the "
+                           "core-only execution of the same schedule");
+    StagedParams sp = P.sp;
+    sp.ro_packed = pack_for(P, repeats);
+    if (dry) {
+      launches = (D.n_items > 0) * (1 + (int)sp.ro_packed);
+    } else {
+    if (core)
       LT_CK(cudaMemsetAsync(P.done.get(), 0, 4 * P.done.n, ctx.stream));
+    else if (P.n_bnd > 0) {
+      k_zero_at<<<grid_for(P.n_bnd, 256), 256, 0, ctx.stream>>>(P.done.get(), P.order_bnd.get(),
+                                                               P.n_bnd);
+      LT_CK_LAUNCH();
+    }
+    P.last_call = core && bnd ? 0 : core ? 1 : 2;
     LT_CK(cudaMemsetAsync(P.queue.get(), 0, 4, ctx.stream));
     // packing costs one pass over the read-only rows: it pays when every tile
     // runs more than once in this call
-    StagedParams sp = P.sp;
-    sp.ro_packed = pack_for(P, repeats);
     if (D.n_items > 0 && sp.ro_packed) {
       k_pack_ro<<<std::min(D.n_exec, 16 * 148), 256, 0, ctx.stream>>>(sp, D.order, D.n_exec);
       LT_CK_LAUNCH();
@@ -2837,6 +2880,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       LT_CK_LAUNCH();
       ++launches;
     }
+    }
     colors = (int)P.phases.size();
   } else {
     for (int r = 0; r < repeats; ++r) {
@@ -2845,13 +2889,15 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
         if (!((reg == LT_CORE && (phases & LT_PHASE_CORE)) ||
               (reg == LT_BOUNDARY && (phases & LT_PHASE_BOUNDARY))))
           continue;
-        if (P.staged)
+        if (dry)
+          ;
+        else if (P.staged)
           staged_fn(fam)<<<P.phases[ph].first, LT_SBLOCK, P.smem_bytes, ctx.stream>>>(
               P.sp, P.phases[ph].second.get());
         else
           fused_fn(fam)<<<P.phases[ph].first, LT_BLOCK, P.smem_bytes, ctx.stream>>>(
               P.dloops.get(), s->n_loops, P.phases[ph].second.get());
-        LT_CK_LAUNCH();
+        if (!dry) LT_CK_LAUNCH();
         ++launches;
         if (r == 0) ++colors;
       }
@@ -3030,6 +3076,16 @@ extern "C" int lt_execute_repeat(lt_ctx *ctx, lt_schedule *s, const lt_chain *ch
   ChainView cv(chain);
   execute_tiled(*ctx, s, cv, args, LT_PHASE_CORE | LT_PHASE_BOUNDARY, use_local_maps ? 1 : 0,
                 repeats, info);
+  LT_API_END
+}
+
+extern "C" int lt_prepare(lt_ctx *ctx, lt_schedule *s, const lt_chain *chain,
+                          const lt_arg *args, int32_t phases, int32_t repeats,
+                          int32_t use_local_maps, lt_exec_info *info) {
+  LT_API_BEGIN
+  if (!ctx || !s || !chain || !args) fail(LT_E_VALUE, "null argument");
+  ChainView cv(chain);
+  execute_tiled(*ctx, s, cv, args, phases, use_local_maps ? 1 : 0, repeats, info, true);
   LT_API_END
 }
 

@@ -101,6 +101,7 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = 0;
   std::map<int, DevBuf<double>> params;  // per native kernel id
+  uint64_t params_gen = 0;                // bumped when a parameter block is reallocated
 };
 
 // ---- host copy of an lt_chain ----------------------------------------------

@@ -175,9 +175,11 @@ class ElasticSetup:
     local_mesh: object = None   # set on rank-local setups
     global_ids: dict | None = None
 
+    num_cells: int | None = None  # device-generated setups carry no host Mesh
+
     @property
     def n_cells(self) -> int:
-        return self.mesh.num_cells
+        return self.mesh.num_cells if self.mesh is not None else self.num_cells
 
     @property
     def dofs(self) -> int:
@@ -204,11 +206,17 @@ def _gaussian_projection(mesh: Mesh, tab: DGTables, centre, sigma: float) -> np.
 def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
                   material="homogeneous", noise_seed: int | None = 1, sigma: float = 8.0,
                   dt: float | None = None, renumbering: str | None = None,
-                  mesh: Mesh | None = None) -> ElasticSetup:
+                  mesh: Mesh | None = None, centre=None,
+                  cell_offset: int = 0) -> ElasticSetup:
     """Build the BASELINE elastic DG instance on an nx x ny right-diagonal mesh (h = 1).
 
     ``material``: "homogeneous" (rho=1, lambda=2, mu=1) or ("uniform", seed) for
     per-cell rho, lambda, mu ~ U[1, 2] drawn as rng.uniform(1, 2, (cells, 3)).
+
+    ``mesh``/``centre``/``cell_offset`` build a window of a larger mesh (the
+    strips of ``strips.py``): the pulse centre is the global one and the random
+    streams are advanced past the ``cell_offset`` cells before the window, so
+    the window's draws are the global draws of its cells.
     """
     tab = dg_tables(p)
     nd = tab.nd
@@ -239,7 +247,9 @@ def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
     else:
         kind, seed = material
         assert kind == "uniform"
-        mat = np.random.default_rng(seed).uniform(1.0, 2.0, size=(C, 3))
+        rng = np.random.default_rng(seed)
+        rng.bit_generator.advance(3 * cell_offset)  # one 64-bit draw per double
+        mat = rng.uniform(1.0, 2.0, size=(C, 3))
     if dt is None:
         cp = np.sqrt((mat[:, 1] + 2 * mat[:, 2]) / mat[:, 0]).max()
         dt = 0.1 * 1.0 / (cp * (2 * p + 1))
@@ -248,11 +258,14 @@ def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
     mat = np.column_stack([mat, zp, zs])
     # initial condition: Gaussian pulse at the domain centre on all components
     X = mesh.vertex_coords
-    centre = ((X[:, 0].min() + X[:, 0].max()) / 2, (X[:, 1].min() + X[:, 1].max()) / 2)
+    if centre is None:
+        centre = ((X[:, 0].min() + X[:, 0].max()) / 2, (X[:, 1].min() + X[:, 1].max()) / 2)
     g = _gaussian_projection(mesh, tab, centre, sigma)
     q = np.repeat(g[:, None, :], 5, axis=1)                # (C, 5, nd)
     if noise_seed is not None:
-        q = q + np.random.default_rng(noise_seed).uniform(-1e-3, 1e-3, size=q.shape)
+        rng = np.random.default_rng(noise_seed)
+        rng.bit_generator.advance(5 * nd * cell_offset)
+        q = q + rng.uniform(-1e-3, 1e-3, size=q.shape)
     data = {
         "cgeo": cgeo.ravel(), "mat": mat.ravel(),
         "u": q[:, 0:2, :].reshape(-1).copy(), "s": q[:, 2:5, :].reshape(-1).copy(),
@@ -266,6 +279,191 @@ def elastic_setup(nx: int, ny: int, p: int, steps_per_chain: int = 1,
     loops, bindings = chain_loops(p, steps_per_chain, spaces, maps)
     return ElasticSetup(p, mesh, steps_per_chain, float(dt), spaces, maps, loops, bindings,
                         data, vpe, space_of, tab, facets=ft)
+
+
+# ---- device-side generation (configs 3-4: 8.4M-67M cells) ---------------------------
+
+def rect_mesh_device(nx: int, ny: int, device) -> dict:
+    """The right-diagonal nx x ny mesh generated on ``device`` (torch), in the
+    numbering of ``mesh.generate_rect_mesh`` + ``facet_topology``.
+
+    Vertex (i, j) = j*(nx+1)+i; quad (i, j) gives lower (v00, v10, v11) = cell
+    2q and upper (v00, v11, v01) = cell 2q+1, q = j*nx+i.  Edges are the sorted
+    unique sides: per vertex, right (v, v+1), up (v, v+nx+1), diagonal
+    (v, v+nx+2) where they exist -- the order ``generate_rect_mesh`` emits.
+    Flanks of each edge in closed form (ascending cell ids, local face
+    0: v0v1, 1: v1v2, 2: v2v0):
+      right of (i, j): upper cell of quad (i, j-1), face 1 | lower of (i, j), face 0
+      up of (i, j):    lower cell of quad (i-1, j), face 1 | upper of (i, j), face 2
+      diagonal:        lower of quad (i, j), face 2        | upper of (i, j), face 0
+    Interior facets are the two-flank edges in edge order, exterior the rest.
+    Returns int64 tensors c2v (C*3), if2c/iface (Fi*2), ef2c/eface (Fe).
+    ``tests/test_dg_device_setup.py`` checks equality with the host generator.
+    """
+    import torch
+    L = dict(dtype=torch.int64, device=device)
+    nvx = nx + 1
+    q = torch.arange(nx * ny, **L)
+    qi, qj = q % nx, q // nx
+    v00 = qj * nvx + qi
+    v10, v01 = v00 + 1, v00 + nvx
+    v11 = v01 + 1
+    c2v = torch.stack([v00, v10, v11, v00, v11, v01], dim=1).reshape(-1)
+    del q, qi, qj, v00, v10, v01, v11
+    nv = nvx * (ny + 1)
+    v = torch.arange(nv, **L)
+    vi, vj = v % nvx, v // nvx
+    del v
+    lower = lambda i, j: 2 * (j * nx + i)
+    neg = torch.full_like(vi, -1)
+    # per vertex, slots (right, up, diagonal): flank a/b (cell or -1) and faces
+    fa = torch.stack([torch.where(vj > 0, lower(vi, vj - 1) + 1, neg),
+                      torch.where(vi > 0, lower(vi - 1, vj), neg),
+                      lower(vi, vj)], dim=1)
+    fb = torch.stack([torch.where(vj < ny, lower(vi, vj), neg),
+                      torch.where(vi < nx, lower(vi, vj) + 1, neg),
+                      lower(vi, vj) + 1], dim=1)
+    has = torch.stack([vi < nx, vj < ny, (vi < nx) & (vj < ny)], dim=1)
+    del vi, vj, neg
+    face_a = torch.tensor([1, 1, 2], **L).expand(nv, 3)
+    face_b = torch.tensor([0, 2, 0], **L).expand(nv, 3)
+    fa, fb = fa[has], fb[has]
+    face_a, face_b = face_a[has], face_b[has]
+    del has
+    inter = (fa >= 0) & (fb >= 0)
+    if2c = torch.stack([fa[inter], fb[inter]], dim=1).reshape(-1)
+    iface = torch.stack([face_a[inter], face_b[inter]], dim=1).reshape(-1)
+    ext = ~inter
+    one = torch.where(fa[ext] >= 0, fa[ext], fb[ext])
+    oneface = torch.where(fa[ext] >= 0, face_a[ext], face_b[ext])
+    return {"nv": nv, "c2v": c2v, "if2c": if2c, "iface": iface, "ef2c": one, "eface": oneface}
+
+
+def _coords_of(v, nx):
+    import torch
+    return torch.stack([(v % (nx + 1)).to(torch.float64), (v // (nx + 1)).to(torch.float64)], -1)
+
+
+def _cell_geometry_device(c2v, nx):
+    import torch
+    X = _coords_of(c2v.reshape(-1, 3), nx)              # (C, 3, 2)
+    xr = (X[:, 1] - X[:, 0]) / 2
+    xs = (X[:, 2] - X[:, 0]) / 2
+    det = xr[:, 0] * xs[:, 1] - xs[:, 0] * xr[:, 1]
+    return torch.stack([xs[:, 1] / det, -xs[:, 0] / det, -xr[:, 1] / det, xr[:, 0] / det, det],
+                       dim=1)
+
+
+def _facet_geometry_device(c2v, cells, faces, faces_b, nx):
+    import torch
+    tri = c2v.reshape(-1, 3)
+    P0 = _coords_of(tri[cells, faces], nx)
+    P1 = _coords_of(tri[cells, (faces + 1) % 3], nx)
+    d = P1 - P0
+    length = torch.hypot(d[:, 0], d[:, 1])
+    fb = torch.full_like(length, -1.0) if faces_b is None else faces_b.to(torch.float64)
+    return torch.stack([d[:, 1] / length, -d[:, 0] / length, length / 2,
+                        faces.to(torch.float64), fb], dim=1)
+
+
+def _gaussian_projection_device(c2v, nx, tab: DGTables, centre, sigma, device):
+    import torch
+    r, s, w = triangle_quadrature(tab.p + 3)
+    psi, _, _ = tab.basis(r, s)
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=device)
+    psi, w = T(psi), T(w)
+    lam = [T(-(r + s) / 2), T((1 + r) / 2), T((1 + s) / 2)]
+    tri = c2v.reshape(-1, 3)
+    C = tri.shape[0]
+    out = torch.empty((C, tab.nd), dtype=torch.float64, device=device)
+    chunk = 1 << 21
+    for c0 in range(0, C, chunk):
+        X = _coords_of(tri[c0:c0 + chunk], nx)
+        x = lam[0] * X[:, 0, 0:1] + lam[1] * X[:, 1, 0:1] + lam[2] * X[:, 2, 0:1]
+        y = lam[0] * X[:, 0, 1:2] + lam[1] * X[:, 1, 1:2] + lam[2] * X[:, 2, 1:2]
+        g = torch.exp(-((x - centre[0]) ** 2 + (y - centre[1]) ** 2) / (2 * sigma ** 2))
+        out[c0:c0 + chunk] = (g * w) @ psi
+    return out
+
+
+def elastic_setup_device(nx: int, ny: int, p: int, steps_per_chain: int = 1,
+                         material="homogeneous", noise_seed: int | None = 1,
+                         sigma: float = 8.0, dt: float | None = None,
+                         device=None) -> ElasticSetup:
+    """:func:`elastic_setup` with the mesh, geometry, material and initial state
+    generated on the GPU (no host mesh: the 67M-cell configuration needs no
+    host pass over its cells).  Same numbering, datasets and chain; maps are
+    device tensors (``MeshMap`` validates and fingerprints them on the device).
+    Random draws (per-cell material, initial noise) use the host generator of
+    :func:`elastic_setup` so both setups draw identical values."""
+    import torch
+    device = torch.device(device if device is not None else "cuda")
+    tab = dg_tables(p)
+    nd = tab.nd
+    m = rect_mesh_device(nx, ny, device)
+    C = 2 * nx * ny
+    Fi, Fe = m["if2c"].numel() // 2, m["ef2c"].numel()
+    spaces = {CELLS: IterationSpace(CELLS, C), IFACETS: IterationSpace(IFACETS, Fi),
+              EFACETS: IterationSpace(EFACETS, Fe), VERTS: IterationSpace(VERTS, m["nv"])}
+    maps = {
+        "c2v": MeshMap("c2v", spaces[CELLS], spaces[VERTS], 3, m["c2v"]),
+        "if2c": MeshMap("if2c", spaces[IFACETS], spaces[CELLS], 2, m["if2c"]),
+        "ef2c": MeshMap("ef2c", spaces[EFACETS], spaces[CELLS], 1, m["ef2c"]),
+    }
+    cgeo = _cell_geometry_device(m["c2v"], nx)
+    rows, faces = m["if2c"].reshape(-1, 2), m["iface"].reshape(-1, 2)
+    fig = _facet_geometry_device(m["c2v"], rows[:, 0], faces[:, 0], faces[:, 1], nx)
+    feg = _facet_geometry_device(m["c2v"], m["ef2c"], m["eface"], None, nx)
+    del rows, faces
+    # impedances on the host (numpy's correctly rounded sqrt, as elastic_setup)
+    if material == "homogeneous":
+        row = np.array([1.0, 2.0, 1.0])
+        cp_max = float(np.sqrt((row[1] + 2 * row[2]) / row[0]))
+        row = np.concatenate([row, [np.sqrt(row[0] * (row[1] + 2 * row[2])),
+                                    np.sqrt(row[0] * row[2])]])
+        mat = torch.from_numpy(row).to(device).repeat(C, 1)
+    else:
+        kind, seed = material
+        assert kind == "uniform"
+        host = np.random.default_rng(seed).uniform(1.0, 2.0, size=(C, 3))
+        cp_max = float(np.sqrt((host[:, 1] + 2 * host[:, 2]) / host[:, 0]).max())
+        host = np.column_stack([host, np.sqrt(host[:, 0] * (host[:, 1] + 2 * host[:, 2])),
+                                np.sqrt(host[:, 0] * host[:, 2])])
+        mat = torch.from_numpy(host).to(device)
+        del host
+    if dt is None:
+        dt = 0.1 * 1.0 / (cp_max * (2 * p + 1))
+    centre = (nx / 2.0, ny / 2.0)
+    g = _gaussian_projection_device(m["c2v"], nx, tab, centre, sigma, device)
+    u = g.repeat(1, 2)                                   # (C, 2*nd): [vx(nd) vy(nd)]
+    s_ = g.repeat(1, 3)
+    del g
+    if noise_seed is not None:
+        # the host draw of elastic_setup, (C, 5, nd) row-major, in cell chunks
+        rng = np.random.default_rng(noise_seed)
+        chunk = 1 << 20
+        for c0 in range(0, C, chunk):
+            n = min(chunk, C - c0)
+            z = torch.from_numpy(rng.uniform(-1e-3, 1e-3, size=(n, 5, nd))).to(device)
+            u[c0:c0 + n] += z[:, 0:2].reshape(n, -1)
+            s_[c0:c0 + n] += z[:, 2:5].reshape(n, -1)
+    data = {
+        "cgeo": cgeo.reshape(-1), "mat": mat.reshape(-1), "u": u.reshape(-1),
+        "s": s_.reshape(-1), "ru": torch.zeros(C * 2 * nd, dtype=torch.float64, device=device),
+        "rs": torch.zeros(C * 3 * nd, dtype=torch.float64, device=device),
+        "figeo": fig.reshape(-1), "fegeo": feg.reshape(-1),
+    }
+    vpe = {"cgeo": 5, "mat": 5, "u": 2 * nd, "s": 3 * nd, "ru": 2 * nd, "rs": 3 * nd,
+           "figeo": 5, "fegeo": 5}
+    space_of = {"cgeo": CELLS, "mat": CELLS, "u": CELLS, "s": CELLS, "ru": CELLS, "rs": CELLS,
+                "figeo": IFACETS, "fegeo": EFACETS}
+    loops, bindings = chain_loops(p, steps_per_chain, spaces, maps)
+    del m
+    # the generator's temporaries go back to the driver: the library allocates
+    # its plan from its own stream-ordered pool, not from torch's cache
+    torch.cuda.empty_cache()
+    return ElasticSetup(p, None, steps_per_chain, float(dt), spaces, maps, loops, bindings,
+                        data, vpe, space_of, tab, num_cells=C)
 
 
 def local_elastic_setup(setup: ElasticSetup, lm) -> ElasticSetup:

@@ -329,7 +329,10 @@ class TiledRunner:
         self.handle = schedule.device_handle(chain)
         self.use_local_maps = use_local_maps
         self.repeats = repeats
-        info = self()  # builds the execution plan outside any capture
+        # build the execution plan outside any capture, without executing the
+        # chain (the datasets are untouched until the first call)
+        info = _lib.prepare(self.handle, self.bound.desc, self.bound.args,
+                            _lib.PHASE_CORE | _lib.PHASE_BOUNDARY, repeats, use_local_maps)
         self.launches_per_call = info.launches
         self.executor = {0: "global", 1: "staged", 2: "dataflow"}[info.staged]
         self.smem_bytes = info.smem_bytes
@@ -359,13 +362,11 @@ class TiledRunner:
         return a.launches + b.launches
 
     def graph(self, repeats: int = 1):
-        """CUDA graph replaying ``repeats`` chain executions back to back."""
+        """CUDA graph replaying ``repeats`` chain executions back to back.
+
+        Capturing executes nothing: the plan was built by the constructor, so
+        the datasets change only when the graph is replayed."""
         import torch
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            self()
-        torch.cuda.current_stream().wait_stream(side)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for _ in range(repeats):

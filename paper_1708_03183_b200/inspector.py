@@ -186,7 +186,7 @@ class Schedule:
             off = np.zeros(len(tiles) + 1, dtype=np.int64)
             np.cumsum(sizes, out=off[1:])
             if off[-1] != n:
-                from .errors import ExecutionError
+                from .errors import StaleScheduleError, ExecutionError
                 raise ExecutionError(f"loop {j}: tiles cover {off[-1]} of {n} elements")
             el = (np.concatenate([t.iteration_lists.get(j, np.empty(0, np.int64))
                                   for t in tiles]) if tiles else np.empty(0, np.int64))
@@ -422,6 +422,24 @@ def find_seed_map(chain: LoopChain) -> MeshMap | None:
         if m.source is seed_space:
             return m
     return None
+
+
+def check_legality_gpu(schedule: Schedule, chain: LoopChain) -> dict:
+    """Legality of ``schedule`` for ``chain`` checked on the GPU at any size.
+
+    Restates the reference's brute-force dependence oracle
+    (``pkg/tests/legality.py:15-151``): returns ``{"pairs": n, "reductions": m}``,
+    the number of distinct cross-loop dependence pairs whose later element runs
+    in a different tile of a colour not above the earlier one's, and of
+    reduction pairs split over distinct tiles of equal colour (0 and 0 for a
+    legal schedule).  ``lt_check_legality`` in include/looptile_cuda.h.
+    """
+    from . import _lib
+    from .errors import StaleScheduleError
+    if schedule.fingerprint != chain.fingerprint:
+        raise StaleScheduleError("schedule was inspected for a different chain")
+    handle = schedule.device_handle(chain)
+    return _lib.check_legality(handle, _lib.ChainDesc(chain, device=handle.ctx.device))
 
 
 def inspect_chain(chain: LoopChain, ts: int, mode: ExecMode) -> Schedule:

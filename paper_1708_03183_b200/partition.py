@@ -172,16 +172,26 @@ def partition_for_ranks(mesh: Mesh, nranks: int, depth: int) -> list[LocalMesh]:
         raise ValueError(f"depth must be >= 1, got {depth}")
     if nranks > mesh.num_cells:
         raise ValueError(f"{nranks} ranks for {mesh.num_cells} cells")
-    C, V, E = mesh.num_cells, mesh.num_vertices, mesh.num_edges
+    C = mesh.num_cells
+    cell_owner = np.empty(C, dtype=np.int64)
+    for r, block in enumerate(np.array_split(np.arange(C), nranks)):
+        cell_owner[block] = r
+    return partition_with_owners(mesh, cell_owner, nranks, depth, range(nranks))
+
+
+def partition_with_owners(mesh: Mesh, cell_owner: np.ndarray, nranks: int, depth: int,
+                          ranks, mirror: bool = True) -> list[LocalMesh]:
+    """The decomposition of :func:`partition_for_ranks` for given cell owners,
+    building the local meshes of ``ranks`` only.  ``strips.strip_local_mesh``
+    runs it on a window of rows around one rank's strip; ``mirror=False``
+    then leaves the neighbour-side column of the exchange tables at -1 (a
+    window does not hold the neighbour's whole local numbering)."""
+    V = mesh.num_vertices
     tri = mesh.cells_to_vertices.reshape(-1, 3)
     pairs = mesh.edges_to_vertices.reshape(-1, 2)
     vc_off, vc_cells = _incidence(tri, V)
     c2e = cell_edge_map(mesh)
     flanks = _edge_flanks(mesh, c2e)
-
-    cell_owner = np.empty(C, dtype=np.int64)
-    for r, block in enumerate(np.array_split(np.arange(C), nranks)):
-        cell_owner[block] = r
     inc_owner = cell_owner[vc_cells]
     vmin = _segment_reduce(inc_owner, vc_off, np.minimum)
     vmax = _segment_reduce(inc_owner, vc_off, np.maximum)
@@ -193,12 +203,12 @@ def partition_for_ranks(mesh: Mesh, nranks: int, depth: int) -> list[LocalMesh]:
     edge_rmin, edge_rmax = vmin[pairs].min(axis=1), vmax[pairs].max(axis=1)
 
     infos = []
-    for r in range(nranks):
+    for r in ranks:
         infos.append(_build_rank(r, depth, tri, pairs, vc_off, vc_cells, flanks, cell_owner,
                                  vertex_owner, edge_owner, (cell_rmin, cell_rmax),
                                  (edge_rmin, edge_rmax), (vmin, vmax), mesh))
     _fill_exchange_tables(infos, nranks, {CELLS: cell_owner, EDGES: edge_owner,
-                                          VERTS: vertex_owner})
+                                          VERTS: vertex_owner}, mirror)
     return [LocalMesh(rank=i["rank"], sizes=i["sizes"], cells_to_vertices=i["c2v"],
                       edges_to_vertices=i["e2v"], vertex_coords=i["coords"],
                       global_ids=i["gids"], exchange_table=i["exchange"],
@@ -268,7 +278,8 @@ def _ranges(lo: np.ndarray, hi: np.ndarray) -> np.ndarray:
     return starts + np.arange(total)
 
 
-def _fill_exchange_tables(infos: list[dict], nranks: int, owners: dict) -> None:
+def _fill_exchange_tables(infos: list[dict], nranks: int, owners: dict,
+                          mirror: bool = True) -> None:
     """Pair every halo copy with its owner, ordered by global id on both sides
     (reference ``partition.py:212-241``)."""
     for space, owner in owners.items():
@@ -279,18 +290,19 @@ def _fill_exchange_tables(infos: list[dict], nranks: int, owners: dict) -> None:
             loc[g] = np.arange(len(g))
             local.append(loc)
         halo = [info["gids"][space][owner[info["gids"][space]] != info["rank"]] for info in infos]
-        for r in range(nranks):
-            for s in range(nranks):
+        for r in range(len(infos)):
+            for s in range(len(infos)):
                 if s == r:
                     continue
-                a = halo[r][owner[halo[r]] == s]          # r holds a copy of s's element
-                b = halo[s][owner[halo[s]] == r]          # s holds a copy of r's element
+                rr, rs = infos[r]["rank"], infos[s]["rank"]
+                a = halo[r][owner[halo[r]] == rs]         # r holds a copy of s's element
+                b = halo[s][owner[halo[s]] == rr]         # s holds a copy of r's element
                 gids = np.union1d(a, b)
                 if not len(gids):
                     continue
                 if np.any(local[s][gids] < 0) or np.any(local[r][gids] < 0):
                     missing = gids[(local[s][gids] < 0) | (local[r][gids] < 0)][0]
                     raise PartitionBugError(
-                        f"{space} {int(missing)} missing on rank {s} but shared with {r}")
-                infos[r]["exchange"][(space, s)] = np.stack(
-                    [local[r][gids], local[s][gids]], axis=1)
+                        f"{space} {int(missing)} missing on rank {rs} but shared with {rr}")
+                there = local[s][gids] if mirror else np.full(len(gids), -1, dtype=np.int64)
+                infos[r]["exchange"][(space, rs)] = np.stack([local[r][gids], there], axis=1)

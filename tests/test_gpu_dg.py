@@ -83,7 +83,7 @@ def test_gpu_dg_repeat_equals_sequential_calls(repeats):
         lt.execute_schedule(s, a.chain, a.bindings, a.datasets, a.registry, use_local_maps=True)
     b = elastic_problem(elastic_setup(40, 30, 1, 1, sigma=5.0))
     s2 = lt.inspect_chain(b.chain, 24, lt.ExecMode.SHARED)
-    TiledRunner(s2, b.chain, b.bindings, b.datasets, b.registry, repeats=repeats)
+    TiledRunner(s2, b.chain, b.bindings, b.datasets, b.registry, repeats=repeats)()
     for n in ("u", "s", "ru", "rs"):
         np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
 
@@ -102,6 +102,7 @@ def test_gpu_dg_repeat_repacks_constants_each_call(p, steps):
     sa = lt.inspect_chain(a.chain, 24, lt.ExecMode.SHARED)
     sb = lt.inspect_chain(b.chain, 24, lt.ExecMode.SHARED)
     runner = TiledRunner(sb, b.chain, b.bindings, b.datasets, b.registry, repeats=2)
+    runner()
     for _ in range(2):
         lt.execute_schedule(sa, a.chain, a.bindings, a.datasets, a.registry, use_local_maps=True)
     for pb in (a, b):  # change the material between calls (rho -> 1.5 rho)
@@ -131,13 +132,14 @@ def test_gpu_dg_queue_orders_equal_sequential_calls(order, monkeypatch):
     if r.executor == "dataflow":
         assert r.queue_order == ("wavefront" if order == "wave" else "colour-major")
     r()
+    r()
     for n in ("u", "s", "ru", "rs"):
         np.testing.assert_array_equal(b.datasets[n].numpy(), a.datasets[n].numpy(), err_msg=n)
 
 
-def test_gpu_dg_wide_register_build_matches_untiled():
-    """P2 two-step tiles large enough that shared memory allows <= 4 CTAs per
-    SM run the 128-register dataflow build; results equal the untiled path."""
+def test_gpu_dg_wide_register_build_matches_untiled(exec_mode):
+    """P2 two-step tiles large enough that shared memory allows <= 3 CTAs per
+    SM run the 168-register dataflow build; results equal the untiled path."""
     from paper_1708_03183_b200.dg import elastic_setup
     from paper_1708_03183_b200.executor import TiledRunner
     mk = lambda: elastic_problem(elastic_setup(64, 48, 2, 2, material=("uniform", 9), sigma=6.0))
@@ -146,7 +148,11 @@ def test_gpu_dg_wide_register_build_matches_untiled():
     s = lt.inspect_chain(b.chain, 32, lt.ExecMode.SHARED)
     b.install_params()
     r = TiledRunner(s, b.chain, b.bindings, b.datasets, b.registry, repeats=3)
-    if r.executor == "dataflow":
+    if exec_mode.startswith("dataflow"):
+        assert r.executor == "dataflow", r.executor
         assert r.wide_build, r.smem_bytes
+    else:
+        assert r.executor == exec_mode, r.executor
+    r()
     for n in ("u", "s"):
         assert rel_err(b.datasets[n].numpy(), a.datasets[n].numpy()) <= RTOL, n

@@ -88,3 +88,40 @@ def test_gpu_determinism():
     a = lt.inspect_chain(chain, 4, lt.ExecMode.SHARED).serialize()
     b = lt.inspect_chain(chain, 4, lt.ExecMode.SHARED).serialize()
     assert a == b
+
+
+def _oracle_violations(chain, s):
+    tile_of = [s.tile_of(j, lp.space.total) for j, lp in enumerate(chain.loops)]
+    colors = {t.id: t.color for t in s.tiles}
+    bad = O.check_legality(chain, tile_of, colors, s.tiles[-1].id)
+    red = sum(1 for b in bad if b.startswith("reduction"))
+    return {"pairs": len(bad) - red, "reductions": red}
+
+
+@pytest.mark.parametrize("case,dims,ren,ts,mode,sub", [
+    ("eight", (8, 4), "none", 4, "shared", None),
+    ("eight", (8, 4), "none", 7, "sequential", None),
+    ("toy", (8, 8), "rcm", 8, "shared", None),
+    ("fig2", (16, 8), "rcm", 16, "shared", None),
+    ("fig2", (16, 8), "rcm", 4, "shared", 2),   # reference emits an illegal schedule here
+    ("fig2", (16, 8), "rcm", 2, "shared", 2),
+    ("dg2s2", (6, 6), "none", 12, "shared", None),
+])
+def test_gpu_legality_checker_matches_oracle(case, dims, ren, ts, mode, sub):
+    """lt_check_legality == the oracle's restatement of pkg/tests/legality.py
+    (violation counts), including the reference's own illegal FIG2 sub-chain
+    schedules, and every tile edit that breaks legality is seen."""
+    _, (chain, _, _, _) = build_case(case, dims, ren)
+    if sub:
+        chain = chain.subchain(0, sub)
+    s = lt.inspect_chain(chain, ts, MODES[mode])
+    want = _oracle_violations(chain, s)
+    assert lt.check_legality_gpu(s, chain) == want
+    if sub:
+        assert want["reductions"] > 0 or want["pairs"] > 0 or ts == 2
+    # break it: give every tile the same colour (all cross-tile dependences violate)
+    for t in s.tiles:
+        t.color = 0
+    want = _oracle_violations(chain, s)
+    assert want["pairs"] + want["reductions"] > 0
+    assert lt.check_legality_gpu(s, chain) == want
