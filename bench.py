@@ -294,6 +294,14 @@ def run_single(args, w, rank, world, local):
     updates_per_step = w.dofs * w.T * chains
     value = updates_per_step * world * args.steps / dev_s
     launches_per_step = runner.launches_per_call * (1 if graph is not None else chains)
+    sched_stats = {"tiles": len(sched.tiles), "colors": len(sched.color_order),
+                   "rounds": sched.recolor_rounds}
+    executor = "untiled" if args.untiled else runner.executor
+    build = None if args.untiled else ("wide (168 regs)" if runner.wide_build
+                                       else "narrow (80 regs)")
+    queue_order = None if args.untiled else runner.queue_order
+    free_b, total_b = torch.cuda.mem_get_info()
+    hbm_used_gb = round((total_b - free_b) / 1e9, 1)
 
     # roofline of the dominant kernel: k_dataflow is the step's only launch when
     # chains_per_step == 1 (with repeats > 1 the step adds k_pack_ro, ~4 %)
@@ -301,22 +309,6 @@ def run_single(args, w, rank, world, local):
     peak, peak_src = measured_peaks()
     achieved = b_chain * chains * args.steps / dev_s / 1e9
     traffic, traffic_src = recorded_traffic(w.config, w.ts)
-
-    # the paper's Omega on B200: the untiled GPU executor on the same problem
-    omega = None
-    if not args.no_omega and not args.untiled and world == 1:
-        try:
-            ur = UntiledRunner(pb.chain, pb.bindings, pb.datasets, pb.registry)
-            ustep = lambda: [ur() for _ in range(chains)]
-            timed(ustep, 1, flush, stream)
-            u_s = timed(ustep, 2, flush, stream)
-            u_rate = updates_per_step * 2 / u_s
-            omega = {"untiled_value": u_rate, "tiled_over_untiled": value / u_rate,
-                     "untiled_launches_per_chain": ur.launches_per_call}
-            del ur
-        except Exception as e:  # memory: the untiled scratch at 67M cells
-            omega = {"untiled_value": None, "error": str(e).splitlines()[0][:160]}
-        torch.cuda.empty_cache()
 
     stated = None
     if args.stated_ts and w.ts_stated and not args.untiled:
@@ -353,6 +345,27 @@ def run_single(args, w, rank, world, local):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d}
         del host
 
+    # the paper's Omega on B200: the untiled GPU executor on the same problem
+    # (run last, after the tiled plan is released: at 67M cells both do not fit)
+    omega = None
+    if not args.no_omega and not args.untiled and world == 1:
+        graph = runner = sched = None  # releases the tiled plan (held by the schedule)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        try:
+            ur = UntiledRunner(pb.chain, pb.bindings, pb.datasets, pb.registry)
+            ustep = lambda: [ur() for _ in range(chains)]
+            timed(ustep, 1, flush, stream)
+            u_s = timed(ustep, 2, flush, stream)
+            u_rate = updates_per_step * 2 / u_s
+            omega = {"untiled_value": u_rate, "tiled_over_untiled": value / u_rate,
+                     "untiled_launches_per_chain": ur.launches_per_call}
+            del ur
+        except Exception as e:  # memory: the untiled facet scratch at 67M cells
+            omega = {"untiled_value": None, "error": str(e).splitlines()[0][:160]}
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, dt, sample, kind = cpu_sample(w, CPU_SAMPLE[w.config])
@@ -369,15 +382,12 @@ def run_single(args, w, rank, world, local):
                        "timesteps_per_chain": w.T, "chains_per_step": chains,
                        "job_chains": w.job_chains, "seed_tile": w.ts,
                        "seed_tile_stated": w.ts_stated, "renumber": "none", "mode": "shared",
-                       "tiles": len(sched.tiles), "colors": len(sched.color_order),
-                       "rounds": sched.recolor_rounds, "setup_s": round(setup_s, 2),
+                       **sched_stats, "setup_s": round(setup_s, 2),
                        "inspect_s": round(inspect_s, 3), "plan_s": round(plan_s, 2),
-                       "executor": "untiled" if args.untiled else runner.executor,
-                       "dataflow_build": None if args.untiled else
-                       ("wide (168 regs)" if runner.wide_build else "narrow (80 regs)"),
-                       "queue_order": None if args.untiled else runner.queue_order,
+                       "executor": executor, "dataflow_build": build,
+                       "queue_order": queue_order,
                        "l2": "flushed between steps (256 MiB write)",
-                       "hbm_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
+                       "hbm_used_gb": hbm_used_gb,
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

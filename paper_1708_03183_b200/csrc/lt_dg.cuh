@@ -23,6 +23,22 @@ struct DGShape {
 // i owns component f*ND + i of u, s, ru, rs), facet kernels one per facet
 // point q < NQ.  Lanes never communicate: each writes its own outputs.
 // L0: R = |J| (div sigma ; C:grad v)   [cgeo R, mat R, u R, s R, ru W, rs W]
+#ifndef LT_VEC_DG
+#define LT_VEC_DG 1  // 16-byte shared/global loads of DoF pairs when ND is even
+#endif
+
+// Rows whose field segments start at even offsets (ND even) and whose base is
+// 16-byte aligned can be read two DoFs per load (LDS.128 / LDG.128): half the
+// load instructions of the contractions, same arithmetic order.
+template <int ND>
+__device__ __forceinline__ bool dg_pairs(const double *a, const double *b) {
+  return LT_VEC_DG && ND % 2 == 0 && ((((uintptr_t)a) | ((uintptr_t)b)) & 15) == 0;
+}
+
+__device__ __forceinline__ double2 ld2(const double *p) {
+  return *reinterpret_cast<const double2 *>(p);
+}
+
 template <int P, class C>
 __device__ __forceinline__ void dg_vol(C &c, int i) {
   constexpr int ND = DGShape<P>::ND;
@@ -34,12 +50,28 @@ __device__ __forceinline__ void dg_vol(C &c, int i) {
   double dr[5], ds[5];
 #pragma unroll
   for (int q = 0; q < 5; ++q) { dr[q] = 0.0; ds[q] = 0.0; }
+  if (dg_pairs<ND>(u, s)) {
 #pragma unroll
-  for (int j = 0; j < ND; ++j) {
-    const double a = __ldg(Sr + j), b = __ldg(Ss + j);
-    const double f[5] = {u[j], u[ND + j], s[j], s[ND + j], s[2 * ND + j]};
+    for (int j = 0; j < ND; j += 2) {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(Sr + j));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(Ss + j));
+      const double2 f0 = ld2(u + j), f1 = ld2(u + ND + j), f2 = ld2(s + j),
+                    f3 = ld2(s + ND + j), f4 = ld2(s + 2 * ND + j);
+      const double fa[5] = {f0.x, f1.x, f2.x, f3.x, f4.x};
+      const double fb[5] = {f0.y, f1.y, f2.y, f3.y, f4.y};
 #pragma unroll
-    for (int q = 0; q < 5; ++q) { dr[q] += a * f[q]; ds[q] += b * f[q]; }
+      for (int q = 0; q < 5; ++q) { dr[q] += a.x * fa[q]; ds[q] += b.x * fa[q]; }
+#pragma unroll
+      for (int q = 0; q < 5; ++q) { dr[q] += a.y * fb[q]; ds[q] += b.y * fb[q]; }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const double a = __ldg(Sr + j), b = __ldg(Ss + j);
+      const double f[5] = {u[j], u[ND + j], s[j], s[ND + j], s[2 * ND + j]};
+#pragma unroll
+      for (int q = 0; q < 5; ++q) { dr[q] += a * f[q]; ds[q] += b * f[q]; }
+    }
   }
   const double rx = g[0], ry = g[1], sx = g[2], sy = g[3], det = g[4];
   const double lam = m[1], mu = m[2], l2m = lam + 2.0 * mu;
@@ -76,14 +108,33 @@ __device__ __forceinline__ void dg_trace(const double *__restrict__ E, int face,
                                          const double *u, const double *s, double t[5]) {
   const double *e = E + (face * NQ + pt) * ND;
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+  if (dg_pairs<ND>(u, s)) {
 #pragma unroll
-  for (int j = 0; j < ND; ++j) {
-    const double w = __ldg(e + j);
-    a0 += w * u[j];
-    a1 += w * u[ND + j];
-    a2 += w * s[j];
-    a3 += w * s[ND + j];
-    a4 += w * s[2 * ND + j];
+    for (int j = 0; j < ND; j += 2) {
+      const double2 w = __ldg(reinterpret_cast<const double2 *>(e + j));
+      const double2 f0 = ld2(u + j), f1 = ld2(u + ND + j), f2 = ld2(s + j),
+                    f3 = ld2(s + ND + j), f4 = ld2(s + 2 * ND + j);
+      a0 += w.x * f0.x;
+      a1 += w.x * f1.x;
+      a2 += w.x * f2.x;
+      a3 += w.x * f3.x;
+      a4 += w.x * f4.x;
+      a0 += w.y * f0.y;
+      a1 += w.y * f1.y;
+      a2 += w.y * f2.y;
+      a3 += w.y * f3.y;
+      a4 += w.y * f4.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const double w = __ldg(e + j);
+      a0 += w * u[j];
+      a1 += w * u[ND + j];
+      a2 += w * s[j];
+      a3 += w * s[ND + j];
+      a4 += w * s[2 * ND + j];
+    }
   }
   t[0] = a0; t[1] = a1; t[2] = a2; t[3] = a3; t[4] = a4;
 }

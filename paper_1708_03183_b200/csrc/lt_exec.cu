@@ -103,27 +103,63 @@ struct FlatCtx {  // untiled: element ids, global scratch
 };
 
 // staged: every dataset row the tile touches lives in shared memory; slots are
-// footprint-local row indices produced by the plan
-struct StagedCtx {
+// footprint-local row indices produced by the plan.  A loop's descriptors are
+// resolved once per loop (resolve_descs: first row, row stride, slot map,
+// arity) into registers, so an item's row address is one shared-memory slot
+// load and one multiply-add (was: three dependent shared loads and two
+// constant-bank loads per descriptor access)
+struct StagedDesc {
+  double *row0;     // first row of the bound dataset in shared memory
+  const int *slot;  // slot map of the descriptor in the tile program
+  int stride;       // shared-memory row stride (doubles)
+  int arity;
+};
+
+__device__ __forceinline__ void resolve_descs(const DLoop &L, const int *sb, double *smem,
+                                              const int *base, const int *B, StagedDesc *D) {
+#pragma unroll
+  for (int d = 0; d < LT_MAX_DESC; ++d)
+    if (d < L.n_desc) {
+      D[d].row0 = smem + base[L.a[d].ds];
+      D[d].slot = B + sb[d];
+      D[d].stride = L.a[d].sstride;
+      D[d].arity = L.a[d].arity;
+    }
+}
+
+#ifndef LT_RESOLVE_MINB
+#define LT_RESOLVE_MINB 3  // builds with <= this many CTAs/SM resolve descriptors per loop
+#endif
+
+// R: descriptors resolved per loop (wide builds: the registers are there); else
+// every access walks the tile program (the 80-register builds, which would spill)
+template <bool R>
+struct StagedCtxT {
   static constexpr bool kRecGeo = false;  // |f|/2 and face read from the facet geometry row
   const DLoop &L;
   int e, pos, lpos;  // pos: position in the tile's list
-  double *smem;
   double *scratch;
+  const StagedDesc *D;
+  double *smem;
   const int *base;   // per staged dataset: first double of its rows in smem
   const int *B;      // tile program in smem
   const int *sbase;  // per descriptor: base of its slot map in B
   __device__ int vpe(int d) const { return L.a[d].vpe; }
-  __device__ int arity(int d) const { return L.a[d].arity; }
+  __device__ int arity(int d) const { return R ? D[d].arity : L.a[d].arity; }
   __device__ const double *params() const { return L.params; }
   __device__ int elem() const { return e; }
   __device__ double *row(int d, int slot) const {
-    return smem + base[L.a[d].ds] + slot * L.a[d].sstride;
+    if constexpr (R) return D[d].row0 + slot * D[d].stride;
+    else return smem + base[L.a[d].ds] + slot * L.a[d].sstride;
   }
-  __device__ const double *rd(int d) const { return row(d, B[sbase[d] + pos]); }
-  __device__ double *wr(int d) const { return row(d, B[sbase[d] + pos]); }
+  __device__ int slot_at(int d, int i) const {
+    if constexpr (R) return D[d].slot[i];
+    else return B[sbase[d] + i];
+  }
+  __device__ const double *rd(int d) const { return row(d, slot_at(d, pos)); }
+  __device__ double *wr(int d) const { return row(d, slot_at(d, pos)); }
   __device__ const double *rdm(int d, int k) const {
-    return row(d, B[sbase[d] + pos * L.a[d].arity + k]);
+    return row(d, slot_at(d, pos * arity(d) + k));
   }
   __device__ double *inc(int d, int k) const {
     const DArg &A = L.a[d];
@@ -623,7 +659,7 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
 
 // Phase 2: gather the datasets the chain writes, run every loop on shared
 // memory, store back the rows this tile wrote.
-template <int FAM, int SB = 1>
+template <int FAM, int SB = 1, bool RES = false>
 __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem,
                                          const int *base) {
   const int *B = reinterpret_cast<const int *>(smem);
@@ -646,6 +682,8 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     const int n = LH[0];
     if (n == 0) continue;
     LT_TSTAMP(t_loop);
+    StagedDesc Dd[LT_MAX_DESC];
+    if constexpr (RES) resolve_descs(L, LH + 2, smem, base, B, Dd);
     if (L.deferred) {  // DG facet loop: records, then lifted ordered apply
       const int CH = L.chunk;
       const int *pb = LH + 2 + L.n_desc;
@@ -655,17 +693,17 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
           constexpr int PP = FAM >= 1 && FAM <= 4 ? FAM : 1;
           if ((L.kernel - K_DG_FIRST) % 5 == 1)
             for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
-              StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+              StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
               dg_iflux<PP>(cx, lane);
             });
           else
             for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
-              StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+              StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
               dg_eflux<PP>(cx, lane);
             });
         } else {
           for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
-            StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+            StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
             dispatch<FAM>(L.kernel, cx, lane);
           });
         }
@@ -687,10 +725,12 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
           // inverse mass and update over the same items, lane-local: one pass
           const DLoop &L2 = P.loops[j + 1];
           const int *LH2 = B + P.loop_pos[j + 1];
+          StagedDesc Dd2[LT_MAX_DESC];
+          if constexpr (RES) resolve_descs(L2, LH2 + 2, smem, base, B, Dd2);
           for_items_s(n, L, [&](int pos, int lane) {
-            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_minv<PP>(cx, lane);
-            StagedCtx cy{L2, 0, pos, 0, smem, scratch, base, B, LH2 + 2};
+            StagedCtxT<RES> cy{L2, 0, pos, 0, scratch, Dd2, smem, base, B, LH2 + 2};
             dg_axpy<PP>(cy, lane);
           });
           ++j;
@@ -700,22 +740,22 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
         }
         if (which == 0)
           for_items_s(n, L, [&](int pos, int lane) {
-            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_vol<PP>(cx, lane);
           });
         else if (which == 3)
           for_items_s(n, L, [&](int pos, int lane) {
-            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_minv<PP>(cx, lane);
           });
         else
           for_items_s(n, L, [&](int pos, int lane) {
-            StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_axpy<PP>(cx, lane);
           });
       } else {
         for_items_s(n, L, [&](int pos, int lane) {
-          StagedCtx cx{L, 0, pos, 0, smem, scratch, base, B, LH + 2};
+          StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
           dispatch<FAM>(L.kernel, cx, lane);
         });
       }
@@ -729,7 +769,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
       LT_TSTAMP(t_body);
       for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
-        StagedCtx cx{L, 0, c0 + lp, lp, smem, scratch, base, B, LH + 2};
+        StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
         dispatch<FAM>(L.kernel, cx, lane);
       });
       LT_TACC(32 + (j < 4 ? j : 3), t_body);
@@ -883,7 +923,7 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
     __syncthreads();
     LT_TACC(3, t_wait);
     LT_TSTAMP(t_tile);
-    run_tile<FAM, 2>(P, t, smem, base);
+    run_tile<FAM, 2, (MINB <= LT_RESOLVE_MINB)>(P, t, smem, base);
     prev = t;
     LT_TACC(4, t_tile);
 #ifdef LT_PHASE_TIMING

@@ -30,11 +30,16 @@ struct Error {
 
 void set_last_error(const std::string &msg);
 
+// a failed call's error is also the thread's "last error": clear it (a
+// non-sticky error such as an out-of-memory allocation must not resurface in
+// the caller's next unrelated CUDA call) before turning it into a status code
 #define LT_CK(call)                                                               \
   do {                                                                            \
     cudaError_t _e = (call);                                                      \
-    if (_e != cudaSuccess)                                                        \
+    if (_e != cudaSuccess) {                                                      \
+      (void)cudaGetLastError();                                                   \
       ::lt::fail(LT_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    }                                                                             \
   } while (0)
 
 #define LT_CK_LAUNCH() LT_CK(cudaGetLastError())

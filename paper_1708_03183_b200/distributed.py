@@ -188,8 +188,9 @@ class HaloExchange:
     """
 
     def __init__(self, local_mesh, datasets: dict, exchanged: tuple[str, ...], group=None,
-                 pack=_gpu_pack, unpack=_gpu_unpack):
+                 pack=_gpu_pack, unpack=_gpu_unpack, staging: bool | None = None):
         import torch
+        import torch.distributed as dist
         self.local_mesh = local_mesh
         self.rank = local_mesh.rank
         self.datasets = datasets
@@ -225,6 +226,19 @@ class HaloExchange:
                                n_send)
             self._recv[nbr] = (recv_parts, torch.empty(max(n_recv, 1), dtype=dtype, device=dev),
                                n_recv)
+        # a transport without device buffers (gloo) moves the packed rows
+        # through pinned host buffers: device pack -> host -> send, receive ->
+        # host -> device unpack (NCCL sends the device buffers directly)
+        if staging is None:
+            staging = dev.type == "cuda" and dist.is_initialized() and \
+                dist.get_backend(group) == "gloo"
+        self.staging = bool(staging)
+        self._host = {}
+        if self.staging:
+            for nbr in self.neighbours:
+                self._host[nbr] = (
+                    torch.empty(max(self._send[nbr][2], 1), dtype=dtype, pin_memory=True),
+                    torch.empty(max(self._recv[nbr][2], 1), dtype=dtype, pin_memory=True))
 
     def begin(self) -> None:
         import torch.distributed as dist
@@ -236,12 +250,17 @@ class HaloExchange:
             for name, k, rows, off in parts:
                 self._pack(self.datasets[name].values, k, rows,
                            buf[off:off + rows.numel() * k])
-            if n:
+            if n and self.staging:
+                host = self._host[nbr][0]
+                host[:n].copy_(buf[:n])      # synchronous: the packed rows are final
+                ops.append(dist.P2POp(dist.isend, host[:n], nbr, group=self.group))
+            elif n:
                 ops.append(dist.P2POp(dist.isend, buf[:n], nbr, group=self.group))
         for nbr in self.neighbours:
             _, buf, n = self._recv[nbr]
             if n:
-                ops.append(dist.P2POp(dist.irecv, buf[:n], nbr, group=self.group))
+                dst = self._host[nbr][1][:n] if self.staging else buf[:n]
+                ops.append(dist.P2POp(dist.irecv, dst, nbr, group=self.group))
         self._work = dist.batch_isend_irecv(ops) if ops else []
 
     def end(self) -> None:
@@ -252,6 +271,8 @@ class HaloExchange:
         moved = 0
         for nbr in self.neighbours:
             parts, buf, n = self._recv[nbr]
+            if n and self.staging:
+                buf[:n].copy_(self._host[nbr][1][:n])  # host buffer is reused next chain
             for name, k, rows, off in parts:
                 self._unpack(self.datasets[name].values, k, rows,
                              buf[off:off + rows.numel() * k])
