@@ -297,8 +297,8 @@ def run_single(args, w, rank, world, local):
     sched_stats = {"tiles": len(sched.tiles), "colors": len(sched.color_order),
                    "rounds": sched.recolor_rounds}
     executor = "untiled" if args.untiled else runner.executor
-    build = None if args.untiled else ("wide (168 regs)" if runner.wide_build
-                                       else "narrow (80 regs)")
+    build = None if args.untiled else ("wide (128 regs, <= 4 CTAs/SM)" if runner.wide_build
+                                       else "narrow (80 regs, 6 CTAs/SM)")
     queue_order = None if args.untiled else runner.queue_order
     free_b, total_b = torch.cuda.mem_get_info()
     hbm_used_gb = round((total_b - free_b) / 1e9, 1)

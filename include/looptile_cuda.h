@@ -141,7 +141,7 @@ typedef struct {
     int32_t staged;      /* 0: global-memory tiles, 1: staged per colour, 2: staged dataflow */
     int32_t smem_bytes;  /* dynamic shared memory per CTA */
     int32_t wave_order;  /* dataflow queue: 1 wavefront (L2-local) order, 0 colour-major */
-    int32_t wide_build;  /* dataflow: 1 when the 168-register build ran (<= 3 CTAs/SM) */
+    int32_t wide_build;  /* dataflow: 1 when the 128-register build ran (<= 4 CTAs/SM) */
 } lt_exec_info;
 
 /* ---- library / context ---------------------------------------------------- */

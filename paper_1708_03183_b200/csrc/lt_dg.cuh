@@ -30,9 +30,12 @@ struct DGShape {
 // Rows whose field segments start at even offsets (ND even) and whose base is
 // 16-byte aligned can be read two DoFs per load (LDS.128 / LDG.128): half the
 // load instructions of the contractions, same arithmetic order.
+// (measured: +1 % at P3 in the 168-register build, -2.4 % at P2; P1 and P4
+// have odd ND; so only ND >= 10)
 template <int ND>
 __device__ __forceinline__ bool dg_pairs(const double *a, const double *b) {
-  return LT_VEC_DG && ND % 2 == 0 && ((((uintptr_t)a) | ((uintptr_t)b)) & 15) == 0;
+  return LT_VEC_DG && ND % 2 == 0 && ND >= 10 &&
+         ((((uintptr_t)a) | ((uintptr_t)b)) & 15) == 0;
 }
 
 __device__ __forceinline__ double2 ld2(const double *p) {

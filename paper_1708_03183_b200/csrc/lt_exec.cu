@@ -12,6 +12,8 @@
 // execute_schedule.  No global atomics, no cross-CTA traffic: equal-coloured
 // tiles touch disjoint written data by construction of the schedule.
 #include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -128,7 +130,10 @@ __device__ __forceinline__ void resolve_descs(const DLoop &L, const int *sb, dou
 }
 
 #ifndef LT_RESOLVE_MINB
-#define LT_RESOLVE_MINB 3  // builds with <= this many CTAs/SM resolve descriptors per loop
+// builds with <= this many CTAs/SM resolve descriptors per loop; off: measured
+// 4.6 % slower at config 3 and 3.4 % at config 4 (168-register build) -- the
+// shorter address chains do not pay for the registers they hold across items
+#define LT_RESOLVE_MINB 0
 #endif
 
 // R: descriptors resolved per loop (wide builds: the registers are there); else
@@ -373,6 +378,7 @@ struct StagedParams {
   int32_t ld_pos;                    // header position of the per-dataset load lists
   int32_t base_pos;                  // header position of the per-dataset row bases
   int32_t n_gather, n_store;         // datasets gathered after the dependency wait / stored back
+  int32_t n_tma;                     // datasets gathered by TMA gather4 (0: none)
   int8_t gather_ds[LT_MAX_STAGED];   // their indices (no per-dataset flag tests in the tile)
   int8_t store_ds[LT_MAX_STAGED];
   int32_t pad;
@@ -381,6 +387,7 @@ struct StagedParams {
   const int32_t *blob_len;           // per tile: ints (multiple of 4)
   StageDS ds[LT_MAX_STAGED];
   DLoop loops[LT_MAX_SLOOPS];
+  CUtensorMap tmap[LT_MAX_STAGED];   // per TMA-gathered dataset: [rows x vpe] f64, box vpe x 1
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -412,6 +419,58 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+}
+
+// the dynamic shared memory of the staged kernels starts 128-byte aligned
+// (TMA destinations); plans reserve the 112 bytes this may skip
+__device__ __forceinline__ double *lt_align128(double *p) {
+  return reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+
+// TMA gather: four rows (global ids r0..r3) of a [rows x vpe] float64 tensor
+// into four consecutive shared-memory rows at dst (UTMALDG gather4 in SASS).
+__device__ __forceinline__ void tma_gather4(double *dst, const CUtensorMap *map, int r0, int r1,
+                                            int r2, int r3, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Full-footprint gathers of the TMA datasets in `list` by warp 0: one
+// expect_tx for all their bytes, then each lane issues gather4s for every 32nd
+// group of four footprint rows (a short tail repeats the last row id: the
+// footprint is padded to four rows).  Every thread later waits on `gbar`.
+__device__ __forceinline__ void tma_gather_list(const StagedParams &P, const int8_t *list, int n,
+                                                const int *B, double *smem, const int *base,
+                                                uint64_t *gbar) {
+  if (threadIdx.x >= 32) return;
+  unsigned bytes = 0;
+  for (int q = 0; q < n; ++q) {
+    const StageDS &S = P.ds[list[q]];
+    if (S.tma && S.load == 1) bytes += (unsigned)((B[2 * S.sp] + 3) & ~3) * S.vpe * 8u;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem use
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(gbar)),
+                 "r"(bytes)
+                 : "memory");
+  }
+  __syncwarp();
+  for (int q = 0; q < n; ++q) {
+    const int d = list[q];
+    const StageDS &S = P.ds[d];
+    if (!(S.tma && S.load == 1)) continue;
+    const int nrow = B[2 * S.sp];
+    const int *idx = B + B[2 * S.sp + 1];
+    double *rows = smem + base[d];
+    for (int g = threadIdx.x * 4; g < nrow; g += 128) {
+      const int last = nrow - 1;
+      tma_gather4(rows + g * S.stride, &P.tmap[d], idx[g], idx[min(g + 1, last)],
+                  idx[min(g + 2, last)], idx[min(g + 3, last)], gbar);
+    }
+  }
 }
 
 // Apply the contributions of one chunk for every INC/WRITE descriptor that
@@ -661,18 +720,23 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
 // memory, store back the rows this tile wrote.
 template <int FAM, int SB = 1, bool RES = false>
 __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *smem,
-                                         const int *base) {
+                                         const int *base, uint64_t *gbar, unsigned &gphase) {
   const int *B = reinterpret_cast<const int *>(smem);
   LT_TSTAMP(t_gather);
+  if (P.n_tma) tma_gather_list(P, P.gather_ds, P.n_gather, B, smem, base, gbar);
   for (int q = 0; q < P.n_gather; ++q) {
     const int d = P.gather_ds[q];
     const StageDS &S = P.ds[d];
     if (S.load == 2)
       gather_rows_listed(S, B, B + B[P.ld_pos + 2 * d + 1], B[P.ld_pos + 2 * d], smem + base[d]);
-    else
+    else if (!S.tma)
       gather_rows(S, B, smem + base[d]);
   }
   cp_async_wait_all();
+  if (P.n_tma) {
+    mbar_wait(gbar, gphase);
+    gphase ^= 1u;
+  }
   __syncthreads();
   LT_TACC(1, t_gather);
   double *scratch = smem + base[P.n_ds];
@@ -800,12 +864,17 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
 template <int FAM>
 __global__ void __launch_bounds__(LT_SBLOCK) k_staged_tiles(const __grid_constant__ StagedParams P,
                                                             const int32_t *__restrict__ tile_ids) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t bar;
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  extern __shared__ __align__(16) double smem_raw[];
+  double *smem = lt_align128(smem_raw);
+  __shared__ __align__(8) uint64_t bar, gbar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&gbar, 1);
+  }
   __syncthreads();
+  unsigned gphase = 0;
   const int *base = tile_prefetch(P, tile_ids[blockIdx.x], smem, &bar, 0);
-  run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base);
+  run_tile<FAM>(P, tile_ids[blockIdx.x], smem, base, &gbar, gphase);
 }
 
 // Pack the rows of the read-only datasets of every tile to be run behind its
@@ -866,11 +935,15 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
 template <int FAM, int MINB>
 __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_constant__ StagedParams P,
                                                         const DataflowArgs D) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(16) double smem_raw[];
+  double *smem = lt_align128(smem_raw);
+  __shared__ __align__(8) uint64_t bar, gbar;
   __shared__ int item;
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
-  unsigned phase = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&gbar, 1);
+  }
+  unsigned phase = 0, gphase = 0;
   // the next queue item is popped one tile ahead, hiding the atomic's latency;
   // a CTA still runs its items in queue order, so waits only target items
   // held by running CTAs and the schedule stays deadlock-free
@@ -923,7 +996,7 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
     __syncthreads();
     LT_TACC(3, t_wait);
     LT_TSTAMP(t_tile);
-    run_tile<FAM, 2, (MINB <= LT_RESOLVE_MINB)>(P, t, smem, base);
+    run_tile<FAM, 2, (MINB <= LT_RESOLVE_MINB)>(P, t, smem, base, &gbar, gphase);
     prev = t;
     LT_TACC(4, t_tile);
 #ifdef LT_PHASE_TIMING
@@ -1808,6 +1881,7 @@ static void build_items(Ctx &ctx, ExecPlan &P, int kind, int repeats, size_t ds_
 }
 
 // ---- tile programs ------------------------------------------------------------------
+static int64_t ds_rows(int64_t n, bool tma);
 struct Section {
   const void *src = nullptr;
   bool u8 = false;
@@ -2075,9 +2149,10 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
         for (int k = 0; k < H.n_ds; ++k) {
           if (H.ds[k].ro != pass) continue;
           acc += acc & H.ds[k].vec;  // 16-byte aligned rows for pair copies
+          if (H.ds[k].tma) acc = (acc + 15) & ~int64_t(15);  // 128-byte aligned for TMA
           hdr[H.base_pos + k] = (int32_t)acc;
           const auto &oh = fps[H.ds[k].sp]->off_host;
-          acc += (int64_t)(oh[t + 1] - oh[t]) * H.ds[k].stride;
+          acc += ds_rows(oh[t + 1] - oh[t], H.ds[k].tma) * H.ds[k].stride;
         }
       hdr[H.base_pos + H.n_ds] = (int32_t)acc;
     }
@@ -2096,8 +2171,9 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       for (int k = 0; k < H.n_ds; ++k) {
         if (!H.ds[k].ro) continue;
         acc += acc & H.ds[k].vec;
+        if (H.ds[k].tma) acc = (acc + 15) & ~int64_t(15);
         const auto &oh = fps[H.ds[k].sp]->off_host;
-        acc += (int64_t)(oh[t + 1] - oh[t]) * H.ds[k].stride;
+        acc += ds_rows(oh[t + 1] - oh[t], H.ds[k].tma) * H.ds[k].stride;
       }
       cur = (2 * acc + 3) / 4 * 4;
     }
@@ -2264,7 +2340,51 @@ static int exec_preference() {
 static bool ds_vec(int v, const double *p) {
   return v % 2 == 0 && reinterpret_cast<uintptr_t>(p) % 16 == 0;
 }
-static int ds_stride(int v, bool vec) { return vec ? (v % 4 == 2 ? v : v + 2) : (v | 1); }
+// TMA gather4 datasets: 16-byte rows (vec), at most 256 doubles wide (TMA box
+// limit); their shared rows are dense (stride = vpe, the layout gather4 writes)
+// and the footprint is padded to a multiple of four rows.  LT_NO_TMA=1: the
+// round-1 layout (stride = 2 mod 4 doubles) and cp.async gathers.
+// A gather4 writes its four rows densely at the box width into 128-byte aligned
+// shared memory: TMA rows are padded to a multiple of four doubles (box wider
+// than the tensor; the extra columns are zero-filled) and every TMA dataset's
+// rows start 128-byte aligned.  Only rows of >= 12 doubles (P2-P3 DoF rows),
+// where the padding is at most two doubles.
+static bool ds_tma(int v, const double *p) {
+  return ds_vec(v, p) && v >= 12 && v <= 256 && !getenv("LT_NO_TMA");
+}
+static int ds_stride(int v, bool vec, bool tma = false) {
+  return tma ? (v + 3) & ~3 : vec ? (v % 4 == 2 ? v : v + 2) : (v | 1);
+}
+static int64_t ds_rows(int64_t n, bool tma) { return tma ? (n + 3) & ~int64_t(3) : n; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    LT_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      fail(LT_E_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [rows x vpe] float64 rows as a 2-D tensor with a one-row box (tile::gather4
+// fetches four rows of it per instruction)
+static void row_tensor_map(CUtensorMap *m, const double *data, int64_t rows, int vpe,
+                           int box_width) {
+  const cuuint64_t dims[2] = {(cuuint64_t)vpe, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)vpe * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_width, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(data), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(LT_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
 
 // Footprints, slot maps and written flags of the staged executor.  Returns
 // false (and leaves the plan untouched) when a footprint exceeds shared memory.
@@ -2326,7 +2446,9 @@ static bool build_stage(Ctx &ctx, lt_schedule *s, const ChainView &cv, const lt_
     size_t r = 0;
     for (size_t k = 0; k < ds_ptr.size(); ++k) {
       const auto &oh = P.fp[ds_space[k]].off_host;
-      r += (size_t)(oh[t + 1] - oh[t]) * ds_stride(ds_vpe[k], ds_vec(ds_vpe[k], ds_ptr[k])) + 1;
+      const bool tma = ds_tma(ds_vpe[k], ds_ptr[k]);
+      r += (size_t)ds_rows(oh[t + 1] - oh[t], tma) *
+               ds_stride(ds_vpe[k], ds_vec(ds_vpe[k], ds_ptr[k]), tma) + (tma ? 16 : 1);
     }
     regions_max = std::max(regions_max, r * sizeof(double));
     P.tile_rows[t] = r * sizeof(double);
@@ -2523,7 +2645,8 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         LT_CK_LAUNCH();
         D.a[d].slot = LP.slots[d].get();
         D.a[d].ds = ds_of[a + d];
-        D.a[d].sstride = ds_stride(D.a[d].vpe, ds_vec(D.a[d].vpe, D.a[d].data));
+        D.a[d].sstride = ds_stride(D.a[d].vpe, ds_vec(D.a[d].vpe, D.a[d].data),
+                                   ds_tma(D.a[d].vpe, D.a[d].data));
       }
     }
     if (!LP.inc_desc.empty()) {
@@ -2594,7 +2717,10 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       H.ds[k].data = ds_ptr[k];
       H.ds[k].vpe = ds_vpe[k];
       H.ds[k].vec = ds_vec(ds_vpe[k], ds_ptr[k]) ? 1 : 0;
-      H.ds[k].stride = ds_stride(ds_vpe[k], H.ds[k].vec);
+      H.ds[k].tma = ds_tma(ds_vpe[k], ds_ptr[k]) ? 1 : 0;
+      H.ds[k].stride = ds_stride(ds_vpe[k], H.ds[k].vec, H.ds[k].tma);
+      if (H.ds[k].tma)
+        row_tensor_map(&H.tmap[k], ds_ptr[k], cv.total(ds_space[k]), ds_vpe[k], H.ds[k].stride);
       const int unit = H.ds[k].vec ? ds_vpe[k] / 2 : ds_vpe[k];  // pairs or doubles per row
       H.ds[k].di = LT_SBLOCK / unit;
       H.ds[k].dc = LT_SBLOCK % unit;
@@ -2666,10 +2792,11 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
     build_load_lists(ctx, s, cv, P, ds_of, ds_space);
-    H.n_gather = H.n_store = 0;
+    H.n_gather = H.n_store = H.n_tma = 0;
     for (int k = 0; k < H.n_ds; ++k) {
       if (!H.ds[k].ro && H.ds[k].load) H.gather_ds[H.n_gather++] = (int8_t)k;
       if (H.ds[k].written) H.store_ds[H.n_store++] = (int8_t)k;
+      if (!H.ds[k].ro && H.ds[k].load == 1 && H.ds[k].tma) ++H.n_tma;
     }
     for (int j = 0; j + 1 < nl; ++j)
       P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j);
@@ -2679,13 +2806,13 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     H.blob = P.blob.get();
     H.blob_off = P.blob_off.get();
     H.blob_len = P.blob_len.get();
-    if (blob_max + P.data_max + scratch_max > kSmemMax) {  // caller falls back
+    if (blob_max + P.data_max + scratch_max + 128 > kSmemMax) {  // caller falls back
       g_last_fit = "tile program " + std::to_string(blob_max) + " B + rows " +
                    std::to_string(P.data_max) + " B + scratch " + std::to_string(scratch_max) +
                    " B > " + std::to_string(kSmemMax) + " B";
       return nullptr;
     }
-    P.smem_bytes = blob_max + P.data_max + scratch_max;
+    P.smem_bytes = blob_max + P.data_max + scratch_max + 128;  // + lt_align128 slack
     P.scratch_bytes = scratch_max;
     if (const char *pad = getenv("LT_SMEM_PAD_KB"))  // diagnostics: force lower occupancy
       P.smem_bytes = std::min(kSmemMax, P.smem_bytes + 1024 * (size_t)atoi(pad));
@@ -2728,7 +2855,11 @@ static StagedFn staged_fn(int fam) {
 
 typedef void (*DataflowFn)(const StagedParams, const DataflowArgs);
 #ifndef LT_WIDE_MINB
-#define LT_WIDE_MINB 3  // CTAs per SM of the wide (168-register at 128 threads) build
+// CTAs per SM of the wide build (128 registers at 128 threads): measured in
+// round 2 against the 168-register <= 3 CTAs/SM build, 4 CTAs/SM at a smaller
+// seed tile win (config 3 ts 16: 13.56 vs 13.94 ms at ts 24; config 4 cut
+// ts 12: 44.6 vs 45.6 ms at ts 16)
+#define LT_WIDE_MINB 4
 #endif
 #ifndef LT_NARROW_MINB
 #define LT_NARROW_MINB 6  // CTAs per SM of the narrow (80-register at 128 threads) build

@@ -76,6 +76,8 @@ struct StageDS {
   uint32_t magic;          // x / vpe == umulhi(x, magic) for x < 2^16 (vpe >= 2)
   int32_t vec;             // even vpe, 16-byte aligned: rows moved as 16-byte pairs
                            // (di, dc, magic then count pairs, vpe / 2 per row)
+  int32_t tma;             // full-footprint gathers by TMA tile::gather4 (vec rows, dense
+                           // shared stride, footprint rounded up to 4 rows)
 };
 
 // x / d for 0 <= x < 2^16, 1 <= d < 256, with magic = 2^32 / d + 1 (host: lt_magic)

@@ -62,11 +62,11 @@ CONFIGS = {
                 job_chains=10, chains_per_step=10, device_setup=False,
                 text="config 2: elastic DG P1 256x256 (131,072 cells), homogeneous, "
                      "1 timestep/chain, 10 timesteps"),
-    3: Workload(3, 2048, 2048, 2, 2, ("uniform", 2), 1, 8.0, ts=24, ts_stated=4096,
+    3: Workload(3, 2048, 2048, 2, 2, ("uniform", 2), 1, 8.0, ts=16, ts_stated=4096,
                 job_chains=50, chains_per_step=1, device_setup=True,
                 text="config 3: elastic DG P2 2048x2048 (8,388,608 cells), per-cell "
                      "rho,lambda,mu ~ U[1,2] (seed 2), 2 timesteps/chain"),
-    4: Workload(4, 8192, 4096, 3, 2, "homogeneous", None, 8.0, ts=16, ts_stated=None,
+    4: Workload(4, 8192, 4096, 3, 2, "homogeneous", None, 8.0, ts=12, ts_stated=None,
                 job_chains=25, chains_per_step=1, device_setup=True,
                 text="config 4: elastic DG P3 8192x4096 (67,108,864 cells), homogeneous, "
                      "Gaussian pulse, 2 timesteps/chain"),

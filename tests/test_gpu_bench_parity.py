@@ -10,7 +10,7 @@ for the step's chains) captured in a CUDA graph, as bench.py runs it.
   the fields within 1e-12 (normwise, reference executor.py:163-169 is
   "untiled sequential execution").
 * config 3 at full size (2048x2048 P2, heterogeneous, T=2) at the tuned seed
-  tile 24 and BASELINE's stated 4096: tiled == GPU untiled (itself pinned to
+  tiles 16 (bench) and 24 and BASELINE's stated 4096: tiled == GPU untiled (itself pinned to
   the reference on the small goldens) within 1e-12, and zero legality
   violations of the schedule at that size.
 * config 4's chain (P3, T=2, homogeneous, no noise) on a 1024x512 cut of the
@@ -85,7 +85,7 @@ def config3_untiled():
     return out
 
 
-@pytest.mark.parametrize("ts", [24, 4096])
+@pytest.mark.parametrize("ts", [16, 24, 4096])
 def test_config3_full_tiled_matches_untiled(config3_untiled, ts):
     import torch
     w = W.workload(3, ts=ts)
@@ -94,8 +94,8 @@ def test_config3_full_tiled_matches_untiled(config3_untiled, ts):
     bad = lt.check_legality_gpu(sched, pb.chain)
     assert bad == {"pairs": 0, "reductions": 0}, bad
     runner = W.tiled_runner(pb, sched, repeats=w.chains_per_step)
-    assert runner.executor == ("dataflow" if ts == 24 else "global")
-    if ts == 24:
+    assert runner.executor == ("dataflow" if ts < 4096 else "global")
+    if ts < 4096:  # the 128-register build (<= 4 CTAs/SM), L2-aware queue order
         assert runner.wide_build and runner.queue_order == "wavefront"
     _run_graph(runner)
     for n in ("u", "s"):

@@ -138,8 +138,8 @@ def test_gpu_dg_queue_orders_equal_sequential_calls(order, monkeypatch):
 
 
 def test_gpu_dg_wide_register_build_matches_untiled(exec_mode):
-    """P2 two-step tiles large enough that shared memory allows <= 3 CTAs per
-    SM run the 168-register dataflow build; results equal the untiled path."""
+    """P2 two-step tiles large enough that shared memory allows <= 4 CTAs per
+    SM run the 128-register dataflow build; results equal the untiled path."""
     from paper_1708_03183_b200.dg import elastic_setup
     from paper_1708_03183_b200.executor import TiledRunner
     mk = lambda: elastic_problem(elastic_setup(64, 48, 2, 2, material=("uniform", 9), sigma=6.0))
