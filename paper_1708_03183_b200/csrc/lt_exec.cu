@@ -421,6 +421,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
       : "memory");
 }
 
+// mbar_wait for the TMA gathers: a transaction that never completes (a byte
+// count that does not match what the copies deliver) traps after ~2^26
+// suspended polls (seconds) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_guarded(uint64_t *bar, unsigned phase) {
+  for (unsigned spins = 0;; ++spins) {
+    unsigned done;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (spins > (1u << 26)) __trap();
+  }
+}
+
 // the dynamic shared memory of the staged kernels starts 128-byte aligned
 // (TMA destinations); plans reserve the 112 bytes this may skip
 __device__ __forceinline__ double *lt_align128(double *p) {
@@ -449,7 +467,8 @@ __device__ __forceinline__ void tma_gather_list(const StagedParams &P, const int
   unsigned bytes = 0;
   for (int q = 0; q < n; ++q) {
     const StageDS &S = P.ds[list[q]];
-    if (S.tma && S.load == 1) bytes += (unsigned)((B[2 * S.sp] + 3) & ~3) * S.vpe * 8u;
+    // a gather4 writes (and counts) four full boxes: stride doubles per row
+    if (S.tma && S.load == 1) bytes += (unsigned)((B[2 * S.sp] + 3) & ~3) * S.stride * 8u;
   }
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem use
@@ -734,7 +753,7 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
   }
   cp_async_wait_all();
   if (P.n_tma) {
-    mbar_wait(gbar, gphase);
+    mbar_wait_guarded(gbar, gphase);
     gphase ^= 1u;
   }
   __syncthreads();
@@ -2348,9 +2367,13 @@ static bool ds_vec(int v, const double *p) {
 // shared memory: TMA rows are padded to a multiple of four doubles (box wider
 // than the tensor; the extra columns are zero-filled) and every TMA dataset's
 // rows start 128-byte aligned.  Only rows of >= 12 doubles (P2-P3 DoF rows),
-// where the padding is at most two doubles.
+// where the padding is at most two doubles.  Opt-in (LT_TMA=1): measured 7 %
+// slower than the 128-thread cp.async gathers at configs 3 and 4 (rows of
+// 96-240 bytes; one warp issues the gather4s after the dependency wait, where
+// every thread issues its cp.async copies in parallel).
 static bool ds_tma(int v, const double *p) {
-  return ds_vec(v, p) && v >= 12 && v <= 256 && !getenv("LT_NO_TMA");
+  static const bool on = getenv("LT_TMA") && atoi(getenv("LT_TMA")) > 0;
+  return on && ds_vec(v, p) && v >= 12 && v <= 256;
 }
 static int ds_stride(int v, bool vec, bool tma = false) {
   return tma ? (v + 3) & ~3 : vec ? (v % 4 == 2 ? v : v + 2) : (v | 1);
