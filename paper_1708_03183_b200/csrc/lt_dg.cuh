@@ -147,20 +147,12 @@ __device__ __forceinline__ void dg_trace(const double *__restrict__ E, int face,
 // executor's deferred apply lifts records per (target, DoF row) and adds them
 // in the reference's (element, k) order.
 
-// L1: interior facets, upwind flux at point q (side a's order; side b's own
-// point is NQ-1-q)   [fgeo R, mat R@2, u R@2, s R@2, ru I@2, rs I@2]
-template <int P, class C>
-__device__ __forceinline__ void dg_iflux(C &c, int q) {
-  constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ;
-  if (q >= NQ) return;
-  const double *g = c.rd(0);
-  const double nx = g[0], ny = g[1];
-  const int fa = (int)g[3], fb = (int)g[4];
-  const double *ma = c.rdm(1, 0), *mb = c.rdm(1, 1);
-  const double *__restrict__ E = c.params();
-  double ta[5], tb[5];
-  dg_trace<ND, NQ>(E, fa, q, c.rdm(2, 0), c.rdm(3, 0), ta);
-  dg_trace<ND, NQ>(E, fb, NQ - 1 - q, c.rdm(2, 1), c.rdm(3, 1), tb);
+// Upwind flux of one interior facet point from the two traces (side a's point
+// q, side b's own point NQ-1-q): per-side corrections ra[f*NQ], rb[f*NQ].
+template <int NQ>
+__device__ __forceinline__ void dg_iflux_point(double nx, double ny, const double *ma,
+                                               const double *mb, const double ta[5],
+                                               const double tb[5], double *ra, double *rb) {
   const double la = ma[1], mua = ma[2], lb = mb[1], mub = mb[2];
   const double zpa = ma[3], zsa = ma[4], zpb = mb[3], zsb = mb[4];  // impedances rho*c_p, rho*c_s
   const double ip = 1.0 / (zpa + zpb), is = 1.0 / (zsa + zsb);
@@ -177,7 +169,6 @@ __device__ __forceinline__ void dg_iflux(C &c, int q) {
   const double dTay = zpa * dvn * ny + zsa * dvt * tny;
   const double dvax = dvn * nx + dvt * tnx, dvay = dvn * ny + dvt * tny;
   const double dna = dvax * nx + dvay * ny;
-  double *ra = c.rec(0) + q, *rb = c.rec(1) + (NQ - 1 - q);
   ra[0] = dTax;
   ra[NQ] = dTay;
   ra[2 * NQ] = la * dna + 2.0 * mua * dvax * nx;
@@ -190,6 +181,23 @@ __device__ __forceinline__ void dg_iflux(C &c, int q) {
   rb[2 * NQ] = lb * dnb - 2.0 * mub * dvbx * nx;
   rb[3 * NQ] = lb * dnb - 2.0 * mub * dvby * ny;
   rb[4 * NQ] = -mub * (dvbx * ny + dvby * nx);
+}
+
+// L1: interior facets, upwind flux at point q (side a's order; side b's own
+// point is NQ-1-q)   [fgeo R, mat R@2, u R@2, s R@2, ru I@2, rs I@2]
+template <int P, class C>
+__device__ __forceinline__ void dg_iflux(C &c, int q) {
+  constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ;
+  if (q >= NQ) return;
+  const double *g = c.rd(0);
+  const double nx = g[0], ny = g[1];
+  const int fa = (int)g[3], fb = (int)g[4];
+  const double *ma = c.rdm(1, 0), *mb = c.rdm(1, 1);
+  const double *__restrict__ E = c.params();
+  double ta[5], tb[5];
+  dg_trace<ND, NQ>(E, fa, q, c.rdm(2, 0), c.rdm(3, 0), ta);
+  dg_trace<ND, NQ>(E, fb, NQ - 1 - q, c.rdm(2, 1), c.rdm(3, 1), tb);
+  dg_iflux_point<NQ>(nx, ny, ma, mb, ta, tb, c.rec(0) + q, c.rec(1) + (NQ - 1 - q));
   if (C::kRecGeo && q == 0) {  // staged records omit |f|/2 and the face (read from fgeo)
     double *r0 = c.rec(0) + 5 * NQ, *r1 = c.rec(1) + 5 * NQ;
     r0[0] = g[2];
@@ -197,6 +205,25 @@ __device__ __forceinline__ void dg_iflux(C &c, int q) {
     r1[0] = g[2];
     r1[1] = g[4];
   }
+}
+
+// Traction-free mirror state at one exterior facet point: corrections r[f*NQ].
+template <int NQ>
+__device__ __forceinline__ void dg_eflux_point(double nx, double ny, const double *m,
+                                               const double t[5], double *r) {
+  const double lam = m[1], mu = m[2];
+  const double izp = 1.0 / m[3], izs = 1.0 / m[4];
+  const double tnx = -ny, tny = nx;
+  const double Tx = t[2] * nx + t[4] * ny, Ty = t[4] * nx + t[3] * ny;
+  const double dvn = -(Tx * nx + Ty * ny) * izp;
+  const double dvt = -(Tx * tnx + Ty * tny) * izs;
+  const double dvx = dvn * nx + dvt * tnx, dvy = dvn * ny + dvt * tny;
+  const double dn = dvx * nx + dvy * ny;
+  r[0] = -Tx;
+  r[NQ] = -Ty;
+  r[2 * NQ] = lam * dn + 2.0 * mu * dvx * nx;
+  r[3 * NQ] = lam * dn + 2.0 * mu * dvy * ny;
+  r[4 * NQ] = mu * (dvx * ny + dvy * nx);
 }
 
 // L2: exterior facets, traction-free mirror state, point q
@@ -211,20 +238,7 @@ __device__ __forceinline__ void dg_eflux(C &c, int q) {
   const double *__restrict__ E = c.params();
   double t[5];
   dg_trace<ND, NQ>(E, fa, q, c.rdm(2, 0), c.rdm(3, 0), t);
-  const double lam = m[1], mu = m[2];
-  const double izp = 1.0 / m[3], izs = 1.0 / m[4];
-  const double tnx = -ny, tny = nx;
-  const double Tx = t[2] * nx + t[4] * ny, Ty = t[4] * nx + t[3] * ny;
-  const double dvn = -(Tx * nx + Ty * ny) * izp;
-  const double dvt = -(Tx * tnx + Ty * tny) * izs;
-  const double dvx = dvn * nx + dvt * tnx, dvy = dvn * ny + dvt * tny;
-  const double dn = dvx * nx + dvy * ny;
-  double *r = c.rec(0) + q;
-  r[0] = -Tx;
-  r[NQ] = -Ty;
-  r[2 * NQ] = lam * dn + 2.0 * mu * dvx * nx;
-  r[3 * NQ] = lam * dn + 2.0 * mu * dvy * ny;
-  r[4 * NQ] = mu * (dvx * ny + dvy * nx);
+  dg_eflux_point<NQ>(nx, ny, m, t, c.rec(0) + q);
   if (C::kRecGeo && q == 0) {
     c.rec(0)[5 * NQ] = g[2];
     c.rec(0)[5 * NQ + 1] = g[3];
@@ -259,6 +273,263 @@ __device__ __forceinline__ void dg_axpy(C &c, int i) {
   s[i] += dt * rs[i];
   s[ND + i] += dt * rs[ND + i];
   s[2 * ND + i] += dt * rs[2 * ND + i];
+}
+
+// ---- grouped work items (shared-memory tile executors) ------------------------------
+// The tile executors run a DG loop as (element, group) items with the element
+// index fastest across lanes: a cell item owns RV DoF rows and reads the cell's
+// fields once for all of them; a facet item owns QF facet points and reads both
+// cells' fields once for all of them.  Per accumulator the summation order is
+// that of the one-row / one-point bodies above (j ascending), so the arithmetic
+// is the same; only the number of shared-memory and table loads per DFMA drops
+// (P3: 9 loads per 40 DFMA instead of 7 per 10).
+template <int P>
+struct DGGroup {
+  static constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ;
+  static constexpr int RV = P == 1 ? 1 : 2;               // DoF rows per cell item
+  static constexpr int GV = (ND + RV - 1) / RV;           // cell items per cell
+  static constexpr int QF = P <= 2 ? NQ : (NQ + 1) / 2;   // facet points per facet item
+  static constexpr int GF = (NQ + QF - 1) / QF;           // facet items per facet
+  static constexpr int RA = P <= 2 ? 3 : 5;               // DoF rows per deferred-apply item
+  static constexpr int GA = (ND + RA - 1) / RA;           // apply items per target
+};
+
+template <int ND>
+__device__ __forceinline__ bool dg_pairs_g(const double *a, const double *b) {
+  return ND % 2 == 0 && ((((uintptr_t)a) | ((uintptr_t)b)) & 15) == 0;
+}
+
+template <int P, class C>
+__device__ __forceinline__ void dg_vol_g(C &c, int g) {
+  constexpr int ND = DGShape<P>::ND, RV = DGGroup<P>::RV;
+  const double *gm = c.rd(0), *m = c.rd(1), *u = c.rd(2), *s = c.rd(3);
+  double *ru = c.wr(4), *rs = c.wr(5);
+  const double *__restrict__ Sr = c.params();
+  const double *__restrict__ Ss = Sr + ND * ND;
+  const int i0 = g * RV;
+  const double *a[RV], *b[RV];  // operator rows (the last group of an odd ND repeats a row)
+  double dr[RV][5], ds[RV][5];
+#pragma unroll
+  for (int r = 0; r < RV; ++r) {
+    const int row = min(i0 + r, ND - 1);
+    a[r] = Sr + row * ND;
+    b[r] = Ss + row * ND;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) { dr[r][q] = 0.0; ds[r][q] = 0.0; }
+  }
+  if (dg_pairs_g<ND>(u, s)) {
+#pragma unroll
+    for (int j = 0; j < ND - 1; j += 2) {
+      const double2 f0 = ld2(u + j), f1 = ld2(u + ND + j), f2 = ld2(s + j),
+                    f3 = ld2(s + ND + j), f4 = ld2(s + 2 * ND + j);
+      const double fa[5] = {f0.x, f1.x, f2.x, f3.x, f4.x};
+      const double fb[5] = {f0.y, f1.y, f2.y, f3.y, f4.y};
+#pragma unroll
+      for (int r = 0; r < RV; ++r) {
+        const double2 x = __ldg(reinterpret_cast<const double2 *>(a[r] + j));
+        const double2 y = __ldg(reinterpret_cast<const double2 *>(b[r] + j));
+#pragma unroll
+        for (int q = 0; q < 5; ++q) { dr[r][q] += x.x * fa[q]; ds[r][q] += y.x * fa[q]; }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) { dr[r][q] += x.y * fb[q]; ds[r][q] += y.y * fb[q]; }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const double f[5] = {u[j], u[ND + j], s[j], s[ND + j], s[2 * ND + j]};
+#pragma unroll
+      for (int r = 0; r < RV; ++r) {
+        const double x = __ldg(a[r] + j), y = __ldg(b[r] + j);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) { dr[r][q] += x * f[q]; ds[r][q] += y * f[q]; }
+      }
+    }
+  }
+  const double rx = gm[0], ry = gm[1], sx = gm[2], sy = gm[3], det = gm[4];
+  const double lam = m[1], mu = m[2], l2m = lam + 2.0 * mu;
+#pragma unroll
+  for (int r = 0; r < RV; ++r) {
+    const int i = i0 + r;
+    if (i < ND) {
+      double dx[5], dy[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        dx[q] = rx * dr[r][q] + sx * ds[r][q];
+        dy[q] = ry * dr[r][q] + sy * ds[r][q];
+      }
+      ru[i] = det * (dx[2] + dy[4]);
+      ru[ND + i] = det * (dx[4] + dy[3]);
+      rs[i] = det * (l2m * dx[0] + lam * dy[1]);
+      rs[ND + i] = det * (lam * dx[0] + l2m * dy[1]);
+      rs[2 * ND + i] = det * mu * (dy[0] + dx[1]);
+    }
+  }
+}
+
+// traces of the 5 fields at QF points pt[k] of `face`, the cell's fields read once
+template <int ND, int NQ, int QF>
+__device__ __forceinline__ void dg_trace_g(const double *__restrict__ E, int face,
+                                           const int (&pt)[QF], const double *u, const double *s,
+                                           double (&t)[QF][5]) {
+  const double *e[QF];
+#pragma unroll
+  for (int k = 0; k < QF; ++k) {
+    e[k] = E + (face * NQ + pt[k]) * ND;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) t[k][f] = 0.0;
+  }
+  if (dg_pairs_g<ND>(u, s)) {
+#pragma unroll
+    for (int j = 0; j < ND - 1; j += 2) {
+      const double2 f0 = ld2(u + j), f1 = ld2(u + ND + j), f2 = ld2(s + j),
+                    f3 = ld2(s + ND + j), f4 = ld2(s + 2 * ND + j);
+#pragma unroll
+      for (int k = 0; k < QF; ++k) {
+        const double2 w = __ldg(reinterpret_cast<const double2 *>(e[k] + j));
+        t[k][0] += w.x * f0.x;
+        t[k][1] += w.x * f1.x;
+        t[k][2] += w.x * f2.x;
+        t[k][3] += w.x * f3.x;
+        t[k][4] += w.x * f4.x;
+        t[k][0] += w.y * f0.y;
+        t[k][1] += w.y * f1.y;
+        t[k][2] += w.y * f2.y;
+        t[k][3] += w.y * f3.y;
+        t[k][4] += w.y * f4.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const double f[5] = {u[j], u[ND + j], s[j], s[ND + j], s[2 * ND + j]};
+#pragma unroll
+      for (int k = 0; k < QF; ++k) {
+        const double w = __ldg(e[k] + j);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) t[k][q] += w * f[q];
+      }
+    }
+  }
+}
+
+// interior facet item: points pg*QF .. pg*QF+QF-1 (side a's order)
+template <int P, class C>
+__device__ __forceinline__ void dg_iflux_g(C &c, int pg) {
+  constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ, QF = DGGroup<P>::QF;
+  static_assert(!C::kRecGeo, "grouped facet items: records without geometry");
+  const double *g = c.rd(0);
+  const double nx = g[0], ny = g[1];
+  const int fa = (int)g[3], fb = (int)g[4];
+  const double *ma = c.rdm(1, 0), *mb = c.rdm(1, 1);
+  const double *__restrict__ E = c.params();
+  const int q0 = pg * QF;
+  int pa[QF], pb[QF];
+#pragma unroll
+  for (int k = 0; k < QF; ++k) {
+    pa[k] = min(q0 + k, NQ - 1);
+    pb[k] = NQ - 1 - pa[k];
+  }
+  double ta[QF][5], tb[QF][5];
+  dg_trace_g<ND, NQ, QF>(E, fa, pa, c.rdm(2, 0), c.rdm(3, 0), ta);
+  dg_trace_g<ND, NQ, QF>(E, fb, pb, c.rdm(2, 1), c.rdm(3, 1), tb);
+  double *ra = c.rec(0), *rb = c.rec(1);
+#pragma unroll
+  for (int k = 0; k < QF; ++k)
+    if (q0 + k < NQ) dg_iflux_point<NQ>(nx, ny, ma, mb, ta[k], tb[k], ra + pa[k], rb + pb[k]);
+}
+
+template <int P, class C>
+__device__ __forceinline__ void dg_eflux_g(C &c, int pg) {
+  constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ, QF = DGGroup<P>::QF;
+  static_assert(!C::kRecGeo, "grouped facet items: records without geometry");
+  const double *g = c.rd(0);
+  const double nx = g[0], ny = g[1];
+  const int fa = (int)g[3];
+  const double *m = c.rdm(1, 0);
+  const double *__restrict__ E = c.params();
+  const int q0 = pg * QF;
+  int pa[QF];
+#pragma unroll
+  for (int k = 0; k < QF; ++k) pa[k] = min(q0 + k, NQ - 1);
+  double t[QF][5];
+  dg_trace_g<ND, NQ, QF>(E, fa, pa, c.rdm(2, 0), c.rdm(3, 0), t);
+  double *r = c.rec(0);
+#pragma unroll
+  for (int k = 0; k < QF; ++k)
+    if (q0 + k < NQ) dg_eflux_point<NQ>(nx, ny, m, t[k], r + pa[k]);
+}
+
+// inverse mass / forward Euler as (cell, field f < 5) items: the ND values of
+// one field, contiguous in the cell's row (16-byte pairs when ND is even)
+template <int P, class C>
+__device__ __forceinline__ void dg_minv_g(C &c, int f) {
+  constexpr int ND = DGShape<P>::ND;
+  const double det = c.rd(0)[4], rho = c.rd(1)[0];
+  const double iu = 1.0 / (rho * det), is = 1.0 / det;
+  double *r = f < 2 ? c.wr(2) + f * ND : c.wr(3) + (f - 2) * ND;
+  const double sc = f < 2 ? iu : is;
+  if (dg_pairs_g<ND>(r, r)) {
+#pragma unroll
+    for (int j = 0; j < ND - 1; j += 2) {
+      double2 v = ld2(r + j);
+      v.x *= sc;
+      v.y *= sc;
+      *reinterpret_cast<double2 *>(r + j) = v;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) r[j] *= sc;
+  }
+}
+
+template <int P, class C>
+__device__ __forceinline__ void dg_axpy_g(C &c, int f) {
+  constexpr int ND = DGShape<P>::ND;
+  const double dt = c.params()[0];
+  double *x = f < 2 ? c.wr(0) + f * ND : c.wr(1) + (f - 2) * ND;
+  const double *r = f < 2 ? c.rd(2) + f * ND : c.rd(3) + (f - 2) * ND;
+  if (dg_pairs_g<ND>(x, r)) {
+#pragma unroll
+    for (int j = 0; j < ND - 1; j += 2) {
+      double2 v = ld2(x + j);
+      const double2 w = ld2(r + j);
+      v.x += dt * w.x;
+      v.y += dt * w.y;
+      *reinterpret_cast<double2 *>(x + j) = v;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) x[j] += dt * r[j];
+  }
+}
+
+// deferred apply of one record to RA rows of its target: the record is read
+// once; acc[r][f] += jf * sum_q LIFT[face][i0+r][q] * corr[f][q]
+template <int P>
+__device__ __forceinline__ void dg_lift_rows_g(const double *__restrict__ params, int face, int i0,
+                                               double jf, const double *rec,
+                                               double (&acc)[DGGroup<P>::RA][5]) {
+  constexpr int ND = DGShape<P>::ND, NQ = DGShape<P>::NQ, RV = DGGroup<P>::RA;
+  const double *__restrict__ LIFT = params + 3 * NQ * ND;
+  double corr[5][NQ];
+#pragma unroll
+  for (int f = 0; f < 5; ++f)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) corr[f][q] = rec[f * NQ + q];
+#pragma unroll
+  for (int r = 0; r < RV; ++r) {
+    const double *Lr = LIFT + (face * ND + min(i0 + r, ND - 1)) * NQ;
+    double a[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const double w = __ldg(Lr + q);
+#pragma unroll
+      for (int f = 0; f < 5; ++f) a[f] += w * corr[f][q];
+    }
+#pragma unroll
+    for (int f = 0; f < 5; ++f) acc[r][f] += jf * a[f];
+  }
 }
 
 template <int P, class C>

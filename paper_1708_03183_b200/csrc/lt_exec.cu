@@ -236,6 +236,32 @@ __device__ __forceinline__ void for_items_s(int cnt, const DLoop &L, F &&f) {
   }
 }
 
+// (element, group) items of cnt elements x groups, element index fastest across
+// lanes (adjacent lanes: adjacent list positions, distinct shared-memory rows)
+template <class F>
+__device__ __forceinline__ void for_flat(int cnt, int groups, F &&f) {
+  const int total = cnt * groups;
+  for (int x = threadIdx.x; x < total; x += LT_SBLOCK) {
+    const int g = groups == 1 ? 0 : x / cnt;
+    f(x - g * cnt, g);
+  }
+}
+
+#ifndef LT_TMA_GATHER
+// 1: compile the TMA tile::gather4 footprint gathers (UTMALDG; then opt-in at run
+// time with LT_TMA=1).  Off by default: measured 7 % slower than the cp.async
+// gathers when used, and its scaffolding (run-time aligned shared-memory base,
+// second mbarrier, tensor maps in the kernel parameters) cost 13-23 % even when
+// unused (config 2: 0.552 -> 0.677 ms; config 4 cut ts 12: 47.9 -> 54.3 ms)
+#define LT_TMA_GATHER 0
+#endif
+
+#ifndef LT_GROUPED
+// DG loops of the shared-memory tile executors as grouped items (lt_dg.cuh), per
+// phase: 1 volume, 2 facet records, 4 deferred apply, 8 inverse mass / update
+#define LT_GROUPED 15
+#endif
+
 // ---- fused tiled executor ------------------------------------------------------
 __device__ __forceinline__ void apply_chunk(const DLoop &L, const IncPlan &P, int gc,
                                             const double *smem) {
@@ -378,7 +404,9 @@ struct StagedParams {
   int32_t ld_pos;                    // header position of the per-dataset load lists
   int32_t base_pos;                  // header position of the per-dataset row bases
   int32_t n_gather, n_store;         // datasets gathered after the dependency wait / stored back
+#if LT_TMA_GATHER
   int32_t n_tma;                     // datasets gathered by TMA gather4 (0: none)
+#endif
   int8_t gather_ds[LT_MAX_STAGED];   // their indices (no per-dataset flag tests in the tile)
   int8_t store_ds[LT_MAX_STAGED];
   int32_t pad;
@@ -387,7 +415,9 @@ struct StagedParams {
   const int32_t *blob_len;           // per tile: ints (multiple of 4)
   StageDS ds[LT_MAX_STAGED];
   DLoop loops[LT_MAX_SLOOPS];
+#if LT_TMA_GATHER
   CUtensorMap tmap[LT_MAX_STAGED];   // per TMA-gathered dataset: [rows x vpe] f64, box vpe x 1
+#endif
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -442,9 +472,14 @@ __device__ __forceinline__ void mbar_wait_guarded(uint64_t *bar, unsigned phase)
 // the dynamic shared memory of the staged kernels starts 128-byte aligned
 // (TMA destinations); plans reserve the 112 bytes this may skip
 __device__ __forceinline__ double *lt_align128(double *p) {
+#if LT_TMA_GATHER
   return reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+#else
+  return p;  // compile-time shared-memory base: addresses fold into the instructions
+#endif
 }
 
+#if LT_TMA_GATHER
 // TMA gather: four rows (global ids r0..r3) of a [rows x vpe] float64 tensor
 // into four consecutive shared-memory rows at dst (UTMALDG gather4 in SASS).
 __device__ __forceinline__ void tma_gather4(double *dst, const CUtensorMap *map, int r0, int r1,
@@ -491,6 +526,8 @@ __device__ __forceinline__ void tma_gather_list(const StagedParams &P, const int
     }
   }
 }
+
+#endif  // LT_TMA_GATHER
 
 // Apply the contributions of one chunk for every INC/WRITE descriptor that
 // shares ordered-gather plan `p` (e.g. ru and rs through if2c): one thread per
@@ -735,6 +772,53 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
   }
 }
 
+// Grouped form: one work item per (unique target, group of RA DoF rows), the
+// target index fastest across lanes; every contributor's record is read once
+// for the item's rows.  Same (element, k) order per target row.
+template <int P>
+__device__ __forceinline__ void apply_deferred_g(const DLoop &L, const int *gc_off,
+                                                 const int *utgt, const int *ut_off,
+                                                 const int *slots, int c, const double *scratch,
+                                                 double *smem, const int *base,
+                                                 const int *fslot) {
+  constexpr int ND = DGShape<P>::ND, RV = DGGroup<P>::RA, GV = DGGroup<P>::GA;
+  const DArg &Au = L.a[4], &As = L.a[5], &Ag = L.a[0];
+  const bool two = Au.arity == 2;
+  double *ru = smem + base[Au.ds], *rs = smem + base[As.ds];
+  const double *geo = smem + base[Ag.ds];
+  const int u0 = gc_off[c], nu = gc_off[c + 1] - u0;
+  for_flat(nu, GV, [&](int q, int g) {
+    const int u = u0 + q, i0 = g * RV;
+    double *du = ru + utgt[u] * Au.sstride, *ds = rs + utgt[u] * As.sstride;
+    double acc[RV][5];
+#pragma unroll
+    for (int r = 0; r < RV; ++r) {
+      const int i = min(i0 + r, ND - 1);
+      acc[r][0] = du[i];
+      acc[r][1] = du[ND + i];
+      acc[r][2] = ds[i];
+      acc[r][3] = ds[ND + i];
+      acc[r][4] = ds[2 * ND + i];
+    }
+    for (int s = ut_off[u], s1 = ut_off[u + 1]; s < s1; ++s) {
+      const int sl = slots[s], lp = two ? sl >> 1 : sl, k = two ? sl & 1 : 0;
+      const double *gf = geo + fslot[lp] * Ag.sstride;  // facet geometry [nx ny |f|/2 fa fb]
+      dg_lift_rows_g<P>(L.params, (int)gf[3 + k], i0, gf[2], scratch + (size_t)sl * L.rec, acc);
+    }
+#pragma unroll
+    for (int r = 0; r < RV; ++r) {
+      const int i = i0 + r;
+      if (i < ND) {
+        du[i] = acc[r][0];
+        du[ND + i] = acc[r][1];
+        ds[i] = acc[r][2];
+        ds[ND + i] = acc[r][3];
+        ds[2 * ND + i] = acc[r][4];
+      }
+    }
+  });
+}
+
 // Phase 2: gather the datasets the chain writes, run every loop on shared
 // memory, store back the rows this tile wrote.
 template <int FAM, int SB = 1, bool RES = false>
@@ -742,7 +826,9 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
                                          const int *base, uint64_t *gbar, unsigned &gphase) {
   const int *B = reinterpret_cast<const int *>(smem);
   LT_TSTAMP(t_gather);
+#if LT_TMA_GATHER
   if (P.n_tma) tma_gather_list(P, P.gather_ds, P.n_gather, B, smem, base, gbar);
+#endif
   for (int q = 0; q < P.n_gather; ++q) {
     const int d = P.gather_ds[q];
     const StageDS &S = P.ds[d];
@@ -752,10 +838,12 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
       gather_rows(S, B, smem + base[d]);
   }
   cp_async_wait_all();
+#if LT_TMA_GATHER
   if (P.n_tma) {
     mbar_wait_guarded(gbar, gphase);
     gphase ^= 1u;
   }
+#endif
   __syncthreads();
   LT_TACC(1, t_gather);
   double *scratch = smem + base[P.n_ds];
@@ -768,13 +856,24 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
     StagedDesc Dd[LT_MAX_DESC];
     if constexpr (RES) resolve_descs(L, LH + 2, smem, base, B, Dd);
     if (L.deferred) {  // DG facet loop: records, then lifted ordered apply
-      const int CH = L.chunk;
+      const int CH = LH[1];  // per-tile chunk (tile program header)
       const int *pb = LH + 2 + L.n_desc;
       for (int c0 = 0, ci = 0; c0 < n; c0 += CH, ++ci) {
         LT_TSTAMP(t_rec);
         if (FAM >= 1 && FAM <= 4) {  // kernel selected once per loop, not per item
           constexpr int PP = FAM >= 1 && FAM <= 4 ? FAM : 1;
-          if ((L.kernel - K_DG_FIRST) % 5 == 1)
+          if (LT_GROUPED & 2) {
+            if ((L.kernel - K_DG_FIRST) % 5 == 1)
+              for_flat(min(CH, n - c0), DGGroup<PP>::GF, [&](int lp, int pg) {
+                StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
+                dg_iflux_g<PP>(cx, pg);
+              });
+            else
+              for_flat(min(CH, n - c0), DGGroup<PP>::GF, [&](int lp, int pg) {
+                StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
+                dg_eflux_g<PP>(cx, pg);
+              });
+          } else if ((L.kernel - K_DG_FIRST) % 5 == 1)
             for_items_s(min(CH, n - c0), L, [&](int lp, int lane) {
               StagedCtxT<RES> cx{L, 0, c0 + lp, lp, scratch, Dd, smem, base, B, LH + 2};
               dg_iflux<PP>(cx, lane);
@@ -793,8 +892,12 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
         __syncthreads();
         LT_TACC(40 + (j < 23 ? j : 23), t_rec);
         // fslot: the chunk's facet-geometry slots (descriptor 0, direct)
-        apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem, base,
-                            B + LH[2] + c0);
+        if constexpr ((LT_GROUPED & 4) && FAM >= 1 && FAM <= 4)
+          apply_deferred_g<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem,
+                                base, B + LH[2] + c0);
+        else
+          apply_deferred<FAM>(L, B + pb[0], B + pb[1], B + pb[2], B + pb[3], ci, scratch, smem,
+                              base, B + LH[2] + c0);
         __syncthreads();
       }
       LT_TACC(8 + (j < 24 ? j : 23), t_loop);
@@ -810,26 +913,49 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
           const int *LH2 = B + P.loop_pos[j + 1];
           StagedDesc Dd2[LT_MAX_DESC];
           if constexpr (RES) resolve_descs(L2, LH2 + 2, smem, base, B, Dd2);
-          for_items_s(n, L, [&](int pos, int lane) {
-            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
-            dg_minv<PP>(cx, lane);
-            StagedCtxT<RES> cy{L2, 0, pos, 0, scratch, Dd2, smem, base, B, LH2 + 2};
-            dg_axpy<PP>(cy, lane);
-          });
+          if (LT_GROUPED & 8)
+            for_flat(n, 5, [&](int pos, int f) {
+              StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
+              dg_minv_g<PP>(cx, f);
+              StagedCtxT<RES> cy{L2, 0, pos, 0, scratch, Dd2, smem, base, B, LH2 + 2};
+              dg_axpy_g<PP>(cy, f);
+            });
+          else
+            for_items_s(n, L, [&](int pos, int lane) {
+              StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
+              dg_minv<PP>(cx, lane);
+              StagedCtxT<RES> cy{L2, 0, pos, 0, scratch, Dd2, smem, base, B, LH2 + 2};
+              dg_axpy<PP>(cy, lane);
+            });
           ++j;
           if (!L2.nobar || (j + 1 < P.n_loops && B[P.loop_pos[j + 1]] == 0)) __syncthreads();
           LT_TACC(8 + (j < 24 ? j : 23), t_loop);
           continue;
         }
-        if (which == 0)
+        if (which == 0 && (LT_GROUPED & 1))
+          for_flat(n, DGGroup<PP>::GV, [&](int pos, int g) {
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
+            dg_vol_g<PP>(cx, g);
+          });
+        else if (which == 0)
           for_items_s(n, L, [&](int pos, int lane) {
             StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_vol<PP>(cx, lane);
+          });
+        else if (which == 3 && (LT_GROUPED & 8))
+          for_flat(n, 5, [&](int pos, int f) {
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
+            dg_minv_g<PP>(cx, f);
           });
         else if (which == 3)
           for_items_s(n, L, [&](int pos, int lane) {
             StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_minv<PP>(cx, lane);
+          });
+        else if (LT_GROUPED & 8)
+          for_flat(n, 5, [&](int pos, int f) {
+            StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
+            dg_axpy_g<PP>(cx, f);
           });
         else
           for_items_s(n, L, [&](int pos, int lane) {
@@ -888,7 +1014,7 @@ __global__ void __launch_bounds__(LT_SBLOCK) k_staged_tiles(const __grid_constan
   __shared__ __align__(8) uint64_t bar, gbar;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
-    mbar_init(&gbar, 1);
+    if (LT_TMA_GATHER) mbar_init(&gbar, 1);
   }
   __syncthreads();
   unsigned gphase = 0;
@@ -960,7 +1086,7 @@ __global__ void __launch_bounds__(LT_SBLOCK, MINB) k_dataflow(const __grid_const
   __shared__ int item;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
-    mbar_init(&gbar, 1);
+    if (LT_TMA_GATHER) mbar_init(&gbar, 1);
   }
   unsigned phase = 0, gphase = 0;
   // the next queue item is popped one tile ahead, hiding the atomic's latency;
@@ -1130,8 +1256,8 @@ static DeferredFn untiled_deferred_fn(int fam) {
 
 // ---- plan building -------------------------------------------------------------------
 __global__ void k_inc_keys(const int32_t *elements, const int32_t *sigma, const int32_t *offsets,
-                           const int32_t *chunk_base, const int32_t *map, int arity, int CH,
-                           int64_t n, uint64_t *keys, int32_t *vals) {
+                           const int32_t *chunk_base, const int32_t *map, int arity, int CH0,
+                           const int32_t *tile_chunk, int64_t n, uint64_t *keys, int32_t *vals) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n * arity) return;
   const int64_t p = i / arity;
@@ -1139,6 +1265,7 @@ __global__ void k_inc_keys(const int32_t *elements, const int32_t *sigma, const 
   const int e = elements[p];
   const int t = sigma[e];
   const int pos = (int)(p - offsets[t]);
+  const int CH = tile_chunk ? tile_chunk[t] : CH0;  // per-tile chunks (staged deferred loops)
   const uint64_t gc = (uint64_t)(chunk_base[t] + pos / CH);
   keys[i] = (gc << 32) | (uint32_t)map[(int64_t)e * arity + k];
   vals[i] = (pos % CH) * arity + k;
@@ -1337,6 +1464,8 @@ struct LoopPlan {
   int scratch_per_pos = 0;  // doubles
   DevBuf<int32_t> chunk_base;
   DevBuf<int32_t> gc_tile;  // staged: tile of each global chunk
+  std::vector<int32_t> tile_chunk_host;  // staged deferred loops: chunk of each tile (else empty)
+  DevBuf<int32_t> tile_chunk;
   std::vector<IncBuffers> inc;  // per apply plan
   std::vector<int> inc_desc;
   std::vector<int> plan_map;    // map of each apply plan
@@ -1371,6 +1500,7 @@ struct ExecPlan {
   size_t scratch_bytes = 0;  // contribution/record scratch per CTA
   std::vector<size_t> tile_rows;   // per tile: dataset-row bytes (diagnostics)
   std::vector<int32_t> tile_blob;  // per tile: tile-program ints (diagnostics)
+  std::vector<int32_t> scratch_base_host;  // per tile: first double of its scratch in smem
   // dataflow
   bool dataflow = false;
   DevBuf<int32_t> order_all, order_core, order_bnd, nbr_off, nbr, done, queue;
@@ -1403,7 +1533,8 @@ static int choose_chunk(int scratch_per_pos, size_t smem_budget, int block, bool
 static void build_inc_plan(Ctx &ctx, const lt_schedule *s, int j, const lt_map &mp, int CH,
                            const std::vector<int32_t> &chunk_base_host,
                            const DevBuf<int32_t> &chunk_base, IncBuffers &out,
-                           const Footprint *fp, const DevBuf<int32_t> *gc_tile) {
+                           const Footprint *fp, const DevBuf<int32_t> *gc_tile,
+                           const int32_t *tile_chunk = nullptr) {
   const LoopLists &Lj = s->lists[j];
   const int64_t n = Lj.n, nnz = n * mp.arity;
   const int64_t n_gc = chunk_base_host.back();
@@ -1420,7 +1551,7 @@ static void build_inc_plan(Ctx &ctx, const lt_schedule *s, int j, const lt_map &
   }
   k_inc_keys<<<grid_for(nnz, 256), 256, 0, ctx.stream>>>(
       Lj.elements.get(), Lj.sigma.get(), Lj.offsets.get(), chunk_base.get(), mp.values, mp.arity,
-      CH, n, kin.get(), vin.get());
+      CH, tile_chunk, n, kin.get(), vin.get());
   LT_CK_LAUNCH();
   sort_pairs_u64(ctx, kin.get(), vin.get(), nnz, 32 + bits_for(n_gc), kout.get(),
                  out.slots.get());
@@ -1591,6 +1722,7 @@ static size_t scratch_budget() {
 }
 static std::string g_last_fit;
 static const size_t kSmemMax = 227 * 1024;
+static const size_t kAlignSlack = LT_TMA_GATHER ? 128 : 0;  // skipped by lt_align128
 
 __global__ void k_zero_at(int32_t *v, const int32_t *idx, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2089,6 +2221,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
   if (P.dataflow) sec(P.nbr.get(), false);
   std::vector<int32_t> hdr(H.hs);
   int n_exec = 0;
+  P.scratch_base_host.assign(nt, 0);
   for (int t = 0; t < nt; ++t) {
     if (s->region[t] == LT_NONEXEC) continue;
     ++n_exec;
@@ -2114,7 +2247,8 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
       int32_t *h = &hdr[H.loop_pos[j]];
       const int32_t o = off[j][t], n = off[j][t + 1] - o;
       h[0] = n;
-      h[1] = cb[j].empty() ? 0 : cb[j][t + 1] - cb[j][t];
+      // elements per chunk of this tile (per-tile for staged deferred loops)
+      h[1] = LP.tile_chunk_host.empty() ? LP.chunk : LP.tile_chunk_host[t];
       const int nd = (int)cv.loops[j].desc.size();
       for (int d = 0; d < nd; ++d) {
         // descriptors with the same map (or all direct ones) share one slot map
@@ -2174,6 +2308,7 @@ static size_t build_blobs(Ctx &ctx, lt_schedule *s, const ChainView &cv, ExecPla
           acc += ds_rows(oh[t + 1] - oh[t], H.ds[k].tma) * H.ds[k].stride;
         }
       hdr[H.base_pos + H.n_ds] = (int32_t)acc;
+      P.scratch_base_host[t] = (int32_t)acc;
     }
     {  // header section
       Section &S = secs[s_hdr];
@@ -2372,7 +2507,7 @@ static bool ds_vec(int v, const double *p) {
 // 96-240 bytes; one warp issues the gather4s after the dependency wait, where
 // every thread issues its cp.async copies in parallel).
 static bool ds_tma(int v, const double *p) {
-  static const bool on = getenv("LT_TMA") && atoi(getenv("LT_TMA")) > 0;
+  static const bool on = LT_TMA_GATHER && getenv("LT_TMA") && atoi(getenv("LT_TMA")) > 0;
   return on && ds_vec(v, p) && v >= 12 && v <= 256;
 }
 static int ds_stride(int v, bool vec, bool tma = false) {
@@ -2380,6 +2515,7 @@ static int ds_stride(int v, bool vec, bool tma = false) {
 }
 static int64_t ds_rows(int64_t n, bool tma) { return tma ? (n + 3) & ~int64_t(3) : n; }
 
+#if LT_TMA_GATHER
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -2408,6 +2544,8 @@ static void row_tensor_map(CUtensorMap *m, const double *data, int64_t rows, int
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(LT_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
+
+#endif  // LT_TMA_GATHER
 
 // Footprints, slot maps and written flags of the staged executor.  Returns
 // false (and leaves the plan untouched) when a footprint exceeds shared memory.
@@ -2583,7 +2721,8 @@ static void build_load_lists(Ctx &ctx, lt_schedule *s, const ChainView &cv, Exec
 static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const ChainView &cv,
                                             const lt_arg *args, int use_local,
                                             bool force_global = false,
-                                            size_t scratch_override = 0) {
+                                            size_t scratch_override = 0,
+                                            const std::vector<int64_t> *tile_budget = nullptr) {
   auto plan = std::make_shared<ExecPlan>();
   ExecPlan &P = *plan;
   const int nl = s->n_loops;
@@ -2678,8 +2817,26 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
                             cudaMemcpyDeviceToHost, ctx.stream));
       LT_CK(cudaStreamSynchronize(ctx.stream));
       std::vector<int32_t> cb(s->n_tiles + 1, 0);
-      for (int t = 0; t < s->n_tiles; ++t)
-        cb[t + 1] = cb[t] + (off[t + 1] - off[t] + LP.chunk - 1) / LP.chunk;
+      if (P.staged && D.deferred && tile_budget) {
+        // per-tile chunks: a tile's scratch starts right behind its own rows, so a
+        // tile smaller than the largest one has room for longer chunks (fewer
+        // records + apply phases); never shorter than the uniform chunk
+        LP.tile_chunk_host.resize(s->n_tiles);
+        for (int t = 0; t < s->n_tiles; ++t) {
+          const int len = off[t + 1] - off[t];
+          const int64_t fit = (*tile_budget)[t] / (int64_t)(sizeof(double) * LP.scratch_per_pos);
+          LP.tile_chunk_host[t] =
+              (int32_t)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(fit, LP.chunk),
+                                                            std::max(len, 1)));
+        }
+        LP.tile_chunk.alloc(s->n_tiles, ctx.stream);
+        LT_CK(cudaMemcpyAsync(LP.tile_chunk.get(), LP.tile_chunk_host.data(),
+                              sizeof(int32_t) * s->n_tiles, cudaMemcpyHostToDevice, ctx.stream));
+      }
+      for (int t = 0; t < s->n_tiles; ++t) {
+        const int ch = LP.tile_chunk_host.empty() ? LP.chunk : LP.tile_chunk_host[t];
+        cb[t + 1] = cb[t] + (off[t + 1] - off[t] + ch - 1) / ch;
+      }
       LP.chunk_base.alloc(s->n_tiles + 1, ctx.stream);
       LT_CK(cudaMemcpyAsync(LP.chunk_base.get(), cb.data(), sizeof(int32_t) * cb.size(),
                             cudaMemcpyHostToDevice, ctx.stream));
@@ -2703,7 +2860,7 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
         const lt_map &mp = cv.maps[LP.plan_map[p]];
         build_inc_plan(ctx, s, j, mp, LP.chunk, cb, LP.chunk_base, LP.inc[p],
                        P.staged ? &P.fp.at(mp.target) : nullptr,
-                       P.staged ? &LP.gc_tile : nullptr);
+                       P.staged ? &LP.gc_tile : nullptr, LP.tile_chunk.get());
       }
       for (size_t i = 0; i < LP.inc_desc.size(); ++i) {
         const int d = LP.inc_desc[i];
@@ -2742,8 +2899,10 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       H.ds[k].vec = ds_vec(ds_vpe[k], ds_ptr[k]) ? 1 : 0;
       H.ds[k].tma = ds_tma(ds_vpe[k], ds_ptr[k]) ? 1 : 0;
       H.ds[k].stride = ds_stride(ds_vpe[k], H.ds[k].vec, H.ds[k].tma);
+#if LT_TMA_GATHER
       if (H.ds[k].tma)
         row_tensor_map(&H.tmap[k], ds_ptr[k], cv.total(ds_space[k]), ds_vpe[k], H.ds[k].stride);
+#endif
       const int unit = H.ds[k].vec ? ds_vpe[k] / 2 : ds_vpe[k];  // pairs or doubles per row
       H.ds[k].di = LT_SBLOCK / unit;
       H.ds[k].dc = LT_SBLOCK % unit;
@@ -2815,11 +2974,16 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
       LT_CK(cudaStreamSynchronize(ctx.stream));
     }
     build_load_lists(ctx, s, cv, P, ds_of, ds_space);
-    H.n_gather = H.n_store = H.n_tma = 0;
+    H.n_gather = H.n_store = 0;
+#if LT_TMA_GATHER
+    H.n_tma = 0;
+#endif
     for (int k = 0; k < H.n_ds; ++k) {
       if (!H.ds[k].ro && H.ds[k].load) H.gather_ds[H.n_gather++] = (int8_t)k;
       if (H.ds[k].written) H.store_ds[H.n_store++] = (int8_t)k;
+#if LT_TMA_GATHER
       if (!H.ds[k].ro && H.ds[k].load == 1 && H.ds[k].tma) ++H.n_tma;
+#endif
     }
     for (int j = 0; j + 1 < nl; ++j)
       P.host_loops[j].nobar = barrier_free_pair(ctx, s, cv, args, j);
@@ -2829,14 +2993,29 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
     H.blob = P.blob.get();
     H.blob_off = P.blob_off.get();
     H.blob_len = P.blob_len.get();
-    if (blob_max + P.data_max + scratch_max + 128 > kSmemMax) {  // caller falls back
+    if (blob_max + P.data_max + scratch_max + kAlignSlack > kSmemMax) {  // caller falls back
       g_last_fit = "tile program " + std::to_string(blob_max) + " B + rows " +
                    std::to_string(P.data_max) + " B + scratch " + std::to_string(scratch_max) +
                    " B > " + std::to_string(kSmemMax) + " B";
       return nullptr;
     }
-    P.smem_bytes = blob_max + P.data_max + scratch_max + 128;  // + lt_align128 slack
+    P.smem_bytes = blob_max + P.data_max + scratch_max + kAlignSlack;  // + lt_align128 slack
     P.scratch_bytes = scratch_max;
+    if (tile_budget) {  // per-tile chunks: the largest (rows + own scratch) of any tile
+      size_t need = 0;
+      for (int t = 0; t < s->n_tiles; ++t) {
+        if (s->region[t] == LT_NONEXEC) continue;
+        size_t sc = 0;
+        for (int j = 0; j < nl; ++j) {
+          const LoopPlan &LP = P.loops[j];
+          const int ch = LP.tile_chunk_host.empty() ? LP.chunk : LP.tile_chunk_host[t];
+          sc = std::max(sc, sizeof(double) * (size_t)LP.scratch_per_pos * ch);
+        }
+        need = std::max(need, sizeof(double) * (size_t)P.scratch_base_host[t] + sc);
+      }
+      if (need + kAlignSlack > kSmemMax) return nullptr;
+      P.smem_bytes = need + kAlignSlack;
+    }
     if (const char *pad = getenv("LT_SMEM_PAD_KB"))  // diagnostics: force lower occupancy
       P.smem_bytes = std::min(kSmemMax, P.smem_bytes + 1024 * (size_t)atoi(pad));
     if (getenv("LT_DEBUG_PLAN")) print_plan_stats(s, P, blob_max, scratch_max);
@@ -2957,10 +3136,27 @@ static std::shared_ptr<ExecPlan> plan_with_occupancy(Ctx &ctx, lt_schedule *s,
       best = sc;
       break;
     }
-  if (best < plan->scratch_bytes + LT_PASS2_MIN) return plan;
-  // the blob grows slightly with longer chunks' plans: leave 1 KB of slack
-  auto p2 = build_plan(ctx, s, cv, args, use_local, false, best - LT_PASS2_SLACK);
-  if (p2 && p2->dataflow && dataflow_occupancy(fam, p2->smem_bytes) >= occ) return p2;
+  if (getenv("LT_UNIFORM_CHUNKS")) {  // round-1/2 behaviour: one chunk size for all tiles
+    if (best < plan->scratch_bytes + LT_PASS2_MIN) return plan;
+    // the blob grows slightly with longer chunks' plans: leave 1 KB of slack
+    auto p2 = build_plan(ctx, s, cv, args, use_local, false, best - LT_PASS2_SLACK);
+    if (p2 && p2->dataflow && dataflow_occupancy(fam, p2->smem_bytes) >= occ) return p2;
+    return plan;
+  }
+  // per-tile chunks.  A tile's scratch begins behind its own program and rows,
+  // so every tile smaller than the largest can hold longer chunks in the same
+  // CTA allocation (half the tiles of a 2-timestep DG chain need under half the
+  // shared memory of the largest); the largest tiles get what the uniform
+  // second pass would have given them
+  for (const LoopPlan &LP : plan->loops)
+    if (LP.scratch_per_pos && !LP.deferred) return plan;  // uniform inc_off scaling
+  const size_t target = fixed + best;
+  std::vector<int64_t> tile_budget(s->n_tiles, 0);
+  for (int t = 0; t < s->n_tiles; ++t)
+    tile_budget[t] = (int64_t)target - (int64_t)kAlignSlack - 256 -
+                     (int64_t)sizeof(double) * plan->scratch_base_host[t];
+  auto p3 = build_plan(ctx, s, cv, args, use_local, false, plan->scratch_bytes, &tile_budget);
+  if (p3 && p3->dataflow && dataflow_occupancy(fam, p3->smem_bytes) >= occ) return p3;
   return plan;
 }
 
