@@ -258,8 +258,15 @@ __device__ __forceinline__ void for_flat(int cnt, int groups, F &&f) {
 
 #ifndef LT_GROUPED
 // DG loops of the shared-memory tile executors as grouped items (lt_dg.cuh), per
-// phase: 1 volume, 2 facet records, 4 deferred apply, 8 inverse mass / update
-#define LT_GROUPED 15
+// phase: 1 volume, 2 facet records, 4 deferred apply, 8 inverse mass / update.
+// Measured (B200, dataflow executor, round 2): the tile phases are latency-bound
+// with one to three rounds of items per thread, so the fine items (one DoF row /
+// one facet point per lane) win for the contractions -- grouped volume, records
+// and apply items are 40-70 % slower per phase at P3 despite 3x fewer shared
+// loads -- while the per-field inverse-mass/update items are 20 % faster
+// (conflict-free 16-byte rows); at P2 grouped volume + apply also gain 1.7 %.
+// (evaluated inside run_tile<FAM, ...>)
+#define LT_GROUPED (FAM == 2 ? 13 : 8)
 #endif
 
 // ---- fused tiled executor ------------------------------------------------------

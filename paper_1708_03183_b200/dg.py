@@ -339,6 +339,48 @@ def rect_mesh_device(nx: int, ny: int, device) -> dict:
     return {"nv": nv, "c2v": c2v, "if2c": if2c, "iface": iface, "ef2c": one, "eface": oneface}
 
 
+def morton_renumber_device(m: dict, nx: int, ny: int) -> dict:
+    """Locality renumbering of a device mesh (north star item 3, the layout
+    pass): quads in Morton (Z-curve) order of (i, j), the two cells of a quad
+    kept adjacent, so ``ts`` consecutive cells form a compact block of quads
+    instead of a one-quad-high strip of the row-major numbering (smaller tile
+    footprints after projection across the chain).  Facet flanks are re-sorted
+    to ascending cell ids (the convention of ``facet_topology``) and facets
+    ordered by their first cell.  Returns the renumbered mesh plus
+    ``old_of_new`` (cells) for permuting per-cell inputs drawn in the
+    generator's order."""
+    import torch
+    dev = m["c2v"].device
+    q = torch.arange(nx * ny, dtype=torch.int64, device=dev)
+
+    def spread(v):  # bit k of v -> bit 2k
+        out = torch.zeros_like(v)
+        for k in range(max(nx, ny).bit_length()):
+            out |= ((v >> k) & 1) << (2 * k)
+        return out
+
+    code = spread(q % nx) | (spread(q // nx) << 1)
+    qs = torch.argsort(code)
+    del code, q
+    old_of_new = torch.stack([2 * qs, 2 * qs + 1], dim=1).reshape(-1)
+    del qs
+    new_of_old = torch.empty_like(old_of_new)
+    new_of_old[old_of_new] = torch.arange(old_of_new.numel(), dtype=torch.int64, device=dev)
+    out = {"nv": m["nv"], "old_of_new": old_of_new}
+    out["c2v"] = m["c2v"].reshape(-1, 3)[old_of_new].reshape(-1)
+    f = new_of_old[m["if2c"]].reshape(-1, 2)
+    fc = m["iface"].reshape(-1, 2)
+    swap = f[:, 0] > f[:, 1]
+    f = torch.where(swap[:, None], f.flip(1), f)
+    fc = torch.where(swap[:, None], fc.flip(1), fc)
+    order = torch.argsort(f[:, 0] * 4 + fc[:, 0])      # first cell, then its face: unique
+    out["if2c"], out["iface"] = f[order].reshape(-1), fc[order].reshape(-1)
+    e = new_of_old[m["ef2c"]]
+    order = torch.argsort(e * 4 + m["eface"])
+    out["ef2c"], out["eface"] = e[order], m["eface"][order]
+    return out
+
+
 def _coords_of(v, nx):
     import torch
     return torch.stack([(v % (nx + 1)).to(torch.float64), (v // (nx + 1)).to(torch.float64)], -1)
@@ -389,7 +431,7 @@ def _gaussian_projection_device(c2v, nx, tab: DGTables, centre, sigma, device):
 def elastic_setup_device(nx: int, ny: int, p: int, steps_per_chain: int = 1,
                          material="homogeneous", noise_seed: int | None = 1,
                          sigma: float = 8.0, dt: float | None = None,
-                         device=None) -> ElasticSetup:
+                         device=None, renumber: str | None = None) -> ElasticSetup:
     """:func:`elastic_setup` with the mesh, geometry, material and initial state
     generated on the GPU (no host mesh: the 67M-cell configuration needs no
     host pass over its cells).  Same numbering, datasets and chain; maps are
@@ -402,6 +444,12 @@ def elastic_setup_device(nx: int, ny: int, p: int, steps_per_chain: int = 1,
     nd = tab.nd
     m = rect_mesh_device(nx, ny, device)
     C = 2 * nx * ny
+    old_of_new = None
+    if renumber == "morton":
+        m = morton_renumber_device(m, nx, ny)
+        old_of_new = m.pop("old_of_new")
+    elif renumber not in (None, "none"):
+        raise ValueError(f"unknown device renumbering {renumber!r}")
     Fi, Fe = m["if2c"].numel() // 2, m["ef2c"].numel()
     spaces = {CELLS: IterationSpace(CELLS, C), IFACETS: IterationSpace(IFACETS, Fi),
               EFACETS: IterationSpace(EFACETS, Fe), VERTS: IterationSpace(VERTS, m["nv"])}
@@ -430,6 +478,8 @@ def elastic_setup_device(nx: int, ny: int, p: int, steps_per_chain: int = 1,
         host = np.column_stack([host, np.sqrt(host[:, 0] * (host[:, 1] + 2 * host[:, 2])),
                                 np.sqrt(host[:, 0] * host[:, 2])])
         mat = torch.from_numpy(host).to(device)
+        if old_of_new is not None:          # drawn per cell of the generator's numbering
+            mat = mat[old_of_new]
         del host
     if dt is None:
         dt = 0.1 * 1.0 / (cp_max * (2 * p + 1))
@@ -442,11 +492,21 @@ def elastic_setup_device(nx: int, ny: int, p: int, steps_per_chain: int = 1,
         # the host draw of elastic_setup, (C, 5, nd) row-major, in cell chunks
         rng = np.random.default_rng(noise_seed)
         chunk = 1 << 20
+        new_of_old = None
+        if old_of_new is not None:
+            new_of_old = torch.empty_like(old_of_new)
+            new_of_old[old_of_new] = torch.arange(C, dtype=torch.int64, device=device)
         for c0 in range(0, C, chunk):
             n = min(chunk, C - c0)
             z = torch.from_numpy(rng.uniform(-1e-3, 1e-3, size=(n, 5, nd))).to(device)
-            u[c0:c0 + n] += z[:, 0:2].reshape(n, -1)
-            s_[c0:c0 + n] += z[:, 2:5].reshape(n, -1)
+            if new_of_old is None:
+                u[c0:c0 + n] += z[:, 0:2].reshape(n, -1)
+                s_[c0:c0 + n] += z[:, 2:5].reshape(n, -1)
+            else:                           # rows of the generator's cells c0..c0+n
+                rows = new_of_old[c0:c0 + n]
+                u[rows] += z[:, 0:2].reshape(n, -1)
+                s_[rows] += z[:, 2:5].reshape(n, -1)
+        del new_of_old
     data = {
         "cgeo": cgeo.reshape(-1), "mat": mat.reshape(-1), "u": u.reshape(-1),
         "s": s_.reshape(-1), "ru": torch.zeros(C * 2 * nd, dtype=torch.float64, device=device),

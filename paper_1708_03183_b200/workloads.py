@@ -43,6 +43,7 @@ class Workload:
     chains_per_step: int        # chains one bench step executes
     device_setup: bool
     text: str
+    renumber: str | None = None  # layout pass of the device generator: None or "morton"
 
     @property
     def cells(self) -> int:
@@ -81,7 +82,8 @@ def workload(config: int, **overrides) -> Workload:
 def build_setup(w: Workload, device=None):
     if w.device_setup:
         return elastic_setup_device(w.nx, w.ny, w.p, w.T, material=w.material,
-                                    noise_seed=w.noise_seed, sigma=w.sigma, device=device)
+                                    noise_seed=w.noise_seed, sigma=w.sigma, device=device,
+                                    renumber=w.renumber)
     return elastic_setup(w.nx, w.ny, w.p, w.T, material=w.material, noise_seed=w.noise_seed,
                          sigma=w.sigma)
 

@@ -23,10 +23,13 @@ ap.add_argument("dims", type=int, nargs="*")
 ap.add_argument("--ts", default="16")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--chains", type=int, default=1)
+ap.add_argument("--renumber", default=None)
 a = ap.parse_args()
 over = {"chains_per_step": a.chains}
 if a.dims:
     over.update(nx=a.dims[0], ny=a.dims[1])
+if a.renumber:
+    over.update(renumber=a.renumber)
 w = W.workload(a.config, **over)
 t0 = time.perf_counter()
 pb = W.build_problem(w)
