@@ -8,7 +8,8 @@ Workloads (``paper_1708_03183_b200/workloads.py``, BASELINE.json configs):
 * default, config 4: DG P3 on the 8192x4096 right-diagonal mesh (67.1M
   cells, 3.36e9 DoFs), homogeneous, Gaussian pulse, two timesteps per chain
   -- the largest elastic-wave configuration and the one BASELINE strong-scales
-  over 1/2/4/8 GPUs.  Generated on the GPU (no host pass over the mesh).
+  over 1/2/4/8 GPUs.  Generated on the GPU (no host pass over the mesh), cells
+  numbered along a Z-curve by the layout pass (``renumber: morton``).
 * config 3: DG P2 2048x2048, heterogeneous, two timesteps per chain
   (``--stated-ts`` also times BASELINE's seed tile 4096).
 * config 2: DG P1 256x256, one timestep per chain, 10 chains per step.
@@ -377,11 +378,13 @@ def run_single(args, w, rank, world, local):
             "metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if w.config == 4 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.text, "p": w.p, "cells": w.cells, "dofs": w.dofs,
                        "timesteps_per_chain": w.T, "chains_per_step": chains,
                        "job_chains": w.job_chains, "seed_tile": w.ts,
-                       "seed_tile_stated": w.ts_stated, "renumber": "none", "mode": "shared",
+                       "seed_tile_stated": w.ts_stated, "renumber": w.renumber or "none",
+                       "mode": "shared",
                        **sched_stats, "setup_s": round(setup_s, 2),
                        "inspect_s": round(inspect_s, 3), "plan_s": round(plan_s, 2),
                        "executor": executor, "dataflow_build": build,

@@ -14,7 +14,11 @@ exactly the same problem, schedule and runner:
 
 ``ts`` is the seed tile the B200 executor is tuned for (one tile per CTA,
 footprint in shared memory); ``ts_stated`` the configuration's own seed tile
-where BASELINE states one.  Inputs larger than a few million cells are
+where BASELINE states one.  ``renumber`` is the layout pass of the device
+generator (north star item 3): "morton" numbers quads along a Z-curve, so a
+seed tile of 16 / 32 cells is a 4x2 / 4x4 block of quads instead of a
+one-quad-high strip of the row-major numbering (measured: config 3 12.89 ->
+12.12 ms, config 4 169.6 -> 162.6 ms per chain).  Inputs larger than a few million cells are
 generated on the GPU (``dg.elastic_setup_device``: same numbering and draws as
 the host generator, tests/test_dg_device_setup.py).
 """
@@ -63,14 +67,16 @@ CONFIGS = {
                 job_chains=10, chains_per_step=10, device_setup=False,
                 text="config 2: elastic DG P1 256x256 (131,072 cells), homogeneous, "
                      "1 timestep/chain, 10 timesteps"),
-    3: Workload(3, 2048, 2048, 2, 2, ("uniform", 2), 1, 8.0, ts=16, ts_stated=4096,
+    3: Workload(3, 2048, 2048, 2, 2, ("uniform", 2), 1, 8.0, ts=32, ts_stated=4096,
                 job_chains=50, chains_per_step=1, device_setup=True,
                 text="config 3: elastic DG P2 2048x2048 (8,388,608 cells), per-cell "
-                     "rho,lambda,mu ~ U[1,2] (seed 2), 2 timesteps/chain"),
-    4: Workload(4, 8192, 4096, 3, 2, "homogeneous", None, 8.0, ts=12, ts_stated=None,
+                     "rho,lambda,mu ~ U[1,2] (seed 2), 2 timesteps/chain",
+                renumber="morton"),
+    4: Workload(4, 8192, 4096, 3, 2, "homogeneous", None, 8.0, ts=16, ts_stated=None,
                 job_chains=25, chains_per_step=1, device_setup=True,
                 text="config 4: elastic DG P3 8192x4096 (67,108,864 cells), homogeneous, "
-                     "Gaussian pulse, 2 timesteps/chain"),
+                     "Gaussian pulse, 2 timesteps/chain",
+                renumber="morton"),
 }
 
 

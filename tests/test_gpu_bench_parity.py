@@ -9,12 +9,14 @@ for the step's chains) captured in a CUDA graph, as bench.py runs it.
   inspector's schedule at ts=32 -- the GPU schedule must be byte-identical and
   the fields within 1e-12 (normwise, reference executor.py:163-169 is
   "untiled sequential execution").
-* config 3 at full size (2048x2048 P2, heterogeneous, T=2) at the tuned seed
-  tiles 16 (bench) and 24 and BASELINE's stated 4096: tiled == GPU untiled (itself pinned to
-  the reference on the small goldens) within 1e-12, and zero legality
-  violations of the schedule at that size.
-* config 4's chain (P3, T=2, homogeneous, no noise) on a 1024x512 cut of the
-  config-4 mesh: tiled == untiled within 1e-12 (the full 67M-cell untiled
+* config 3 at full size (2048x2048 P2, heterogeneous, T=2) as benchmarked
+  (Morton layout pass, seed tile 32), at BASELINE's stated seed tile 4096 and in
+  the generator's row-major numbering (seed tile 24): tiled == GPU untiled
+  (itself pinned to the reference on the small goldens) within 1e-12, and zero
+  legality violations of the schedule at that size.
+* config 4's chain as benchmarked (P3, T=2, homogeneous, no noise, Morton
+  layout pass, seed tile 16) on a 1024x512 cut of the config-4 mesh: tiled ==
+  untiled within 1e-12 (the full 67M-cell untiled
   executor does not fit next to the tiled state; bench.py runs the full size).
 """
 
@@ -76,19 +78,28 @@ def test_config2_full_untiled_matches_reference_golden():
         assert rel(v[g["rows"]], g[f"{n}_rows"]) <= RTOL, n
 
 
-@pytest.fixture(scope="module")
-def config3_untiled():
-    pb = W.build_problem(W.workload(3))
-    pb.run_untiled(n_chains=1)
-    out = {n: pb.datasets[n].numpy() for n in ("u", "s")}
-    del pb
-    return out
+_C3_UNTILED = {}
 
 
-@pytest.mark.parametrize("ts", [16, 24, 4096])
-def test_config3_full_tiled_matches_untiled(config3_untiled, ts):
+def config3_untiled(renumber):
+    """GPU untiled result of config 3 in the given numbering (computed once)."""
+    if renumber not in _C3_UNTILED:
+        pb = W.build_problem(W.workload(3, renumber=renumber))
+        pb.run_untiled(n_chains=1)
+        _C3_UNTILED[renumber] = {n: pb.datasets[n].numpy() for n in ("u", "s")}
+        del pb
+    return _C3_UNTILED[renumber]
+
+
+@pytest.mark.parametrize("renumber,ts", [("morton", 32), ("morton", 4096), (None, 24)])
+def test_config3_full_tiled_matches_untiled(renumber, ts):
+    """Bench configuration (Morton layout pass, seed tile 32), BASELINE's stated
+    seed tile 4096, and the generator's row-major numbering at its best tile."""
     import torch
-    w = W.workload(3, ts=ts)
+    ref = config3_untiled(renumber)
+    w = W.workload(3, ts=ts, renumber=renumber)
+    if (renumber, ts) == ("morton", 32):
+        assert (w.ts, w.renumber) == (W.workload(3).ts, W.workload(3).renumber)
     pb = W.build_problem(w)
     sched = lt.inspect_chain(pb.chain, ts, lt.ExecMode.SHARED)
     bad = lt.check_legality_gpu(sched, pb.chain)
@@ -99,7 +110,7 @@ def test_config3_full_tiled_matches_untiled(config3_untiled, ts):
         assert runner.wide_build and runner.queue_order == "wavefront"
     _run_graph(runner)
     for n in ("u", "s"):
-        assert rel(pb.datasets[n].numpy(), config3_untiled[n]) <= RTOL, (n, ts)
+        assert rel(pb.datasets[n].numpy(), ref[n]) <= RTOL, (n, ts)
     del runner, pb
     torch.cuda.empty_cache()
 

@@ -3,7 +3,8 @@
 usage: compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 Runs the dataflow tile executor (and the staged/global/untiled ones) on:
 toy 32x32 (BASELINE config 1), FIG2 16x8 RCM, DG P1 one-step chains repeated
-in one persistent launch, DG P2 two-step chains in wavefront queue order,
+in one persistent launch, DG P2 two-step chains in wavefront queue order, a DG P3
+two-step chain (per-tile record chunks),
 and a 2-virtual-rank partitioned DG chain (core-only + boundary-only calls).
 Each result is checked (bitwise or 1e-12) so the run also proves the
 instrumented kernels computed the right thing.  Exit code 0 = all checks ok.
@@ -78,6 +79,7 @@ if __name__ == "__main__":
         toy_and_fig2(mode)
     dg(1, 1, 3, "colour")
     dg(2, 2, 2, "wave")
+    dg(3, 2, 1, "colour")  # per-tile record chunks, grouped inverse-mass/update items
     distributed()
     torch.cuda.synchronize()
     print("sanitize cases ok")
