@@ -247,6 +247,10 @@ __device__ __forceinline__ void for_flat(int cnt, int groups, F &&f) {
   }
 }
 
+#ifndef LT_APPLY_BATCH
+#define LT_APPLY_BATCH 3  // contributors of a deferred-apply item whose index chains overlap
+#endif
+
 #ifndef LT_TMA_GATHER
 // 1: compile the TMA tile::gather4 footprint gathers (UTMALDG; then opt-in at run
 // time with LT_TMA=1).  Off by default: measured 7 % slower than the cp.async
@@ -762,12 +766,36 @@ __device__ __forceinline__ void apply_deferred(const DLoop &L, const int *gc_off
     const int u = u0 + q;
     double *du = ru + utgt[u] * Au.sstride + i, *ds = rs + utgt[u] * As.sstride + i;
     double acc[5] = {du[0], du[nd], ds[0], ds[nd], ds[2 * nd]};
+#if LT_APPLY_BATCH > 1
+    // contributors in batches: the slot -> facet slot -> geometry row -> (|f|/2,
+    // face) chains of a batch are independent loads issued together (a cell has
+    // three facets: one batch), the lifts then add in (element, k) order
+    for (int s = ut_off[u], s1 = ut_off[u + 1]; s < s1; s += LT_APPLY_BATCH) {
+      int sl[LT_APPLY_BATCH], face[LT_APPLY_BATCH];
+      double jf[LT_APPLY_BATCH];
+#pragma unroll
+      for (int b = 0; b < LT_APPLY_BATCH; ++b) sl[b] = slots[min(s + b, s1 - 1)];
+#pragma unroll
+      for (int b = 0; b < LT_APPLY_BATCH; ++b) {
+        const int lp = two ? sl[b] >> 1 : sl[b], k = two ? sl[b] & 1 : 0;
+        const double *g = geo + fslot[lp] * Ag.sstride;  // facet geometry [nx ny |f|/2 fa fb]
+        jf[b] = g[2];
+        face[b] = (int)g[3 + k];
+      }
+#pragma unroll
+      for (int b = 0; b < LT_APPLY_BATCH; ++b)
+        if (s + b < s1)
+          dg_lift_acc_g<FAM>(L.kernel - K_DG_FIRST, L.params, i, scratch + (size_t)sl[b] * L.rec,
+                             jf[b], face[b], acc);
+    }
+#else
     for (int s = ut_off[u], s1 = ut_off[u + 1]; s < s1; ++s) {
       const int sl = slots[s], lp = two ? sl >> 1 : sl, k = two ? sl & 1 : 0;
       const double *g = geo + fslot[lp] * Ag.sstride;  // facet geometry [nx ny |f|/2 fa fb]
       dg_lift_acc_g<FAM>(L.kernel - K_DG_FIRST, L.params, i, scratch + (size_t)sl * L.rec, g[2],
                          (int)g[3 + k], acc);
     }
+#endif
     du[0] = acc[0];
     du[nd] = acc[1];
     ds[0] = acc[2];
@@ -807,11 +835,31 @@ __device__ __forceinline__ void apply_deferred_g(const DLoop &L, const int *gc_o
       acc[r][3] = ds[ND + i];
       acc[r][4] = ds[2 * ND + i];
     }
+#if LT_APPLY_BATCH > 1
+    for (int s = ut_off[u], s1 = ut_off[u + 1]; s < s1; s += LT_APPLY_BATCH) {
+      int sl[LT_APPLY_BATCH], face[LT_APPLY_BATCH];
+      double jf[LT_APPLY_BATCH];
+#pragma unroll
+      for (int b = 0; b < LT_APPLY_BATCH; ++b) sl[b] = slots[min(s + b, s1 - 1)];
+#pragma unroll
+      for (int b = 0; b < LT_APPLY_BATCH; ++b) {
+        const int lp = two ? sl[b] >> 1 : sl[b], k = two ? sl[b] & 1 : 0;
+        const double *gf = geo + fslot[lp] * Ag.sstride;  // facet geometry [nx ny |f|/2 fa fb]
+        jf[b] = gf[2];
+        face[b] = (int)gf[3 + k];
+      }
+#pragma unroll
+      for (int b = 0; b < LT_APPLY_BATCH; ++b)
+        if (s + b < s1)
+          dg_lift_rows_g<P>(L.params, face[b], i0, jf[b], scratch + (size_t)sl[b] * L.rec, acc);
+    }
+#else
     for (int s = ut_off[u], s1 = ut_off[u + 1]; s < s1; ++s) {
       const int sl = slots[s], lp = two ? sl >> 1 : sl, k = two ? sl & 1 : 0;
       const double *gf = geo + fslot[lp] * Ag.sstride;  // facet geometry [nx ny |f|/2 fa fb]
       dg_lift_rows_g<P>(L.params, (int)gf[3 + k], i0, gf[2], scratch + (size_t)sl * L.rec, acc);
     }
+#endif
 #pragma unroll
     for (int r = 0; r < RV; ++r) {
       const int i = i0 + r;
