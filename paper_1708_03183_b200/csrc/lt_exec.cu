@@ -248,7 +248,11 @@ __device__ __forceinline__ void for_flat(int cnt, int groups, F &&f) {
 }
 
 #ifndef LT_APPLY_BATCH
-#define LT_APPLY_BATCH 3  // contributors of a deferred-apply item whose index chains overlap
+// > 1: a deferred-apply item resolves the slot -> facet -> geometry chains of
+// that many contributors before lifting them (independent loads in flight).
+// Measured slower (3: config 4 cut 40.78 -> 41.36 ms, config 3 12.17 -> 12.34 ms:
+// the extra live registers cost more than the overlapped loads save); off
+#define LT_APPLY_BATCH 1
 #endif
 
 #ifndef LT_TMA_GATHER
