@@ -460,6 +460,91 @@ __device__ __forceinline__ void dg_eflux_g(C &c, int pg) {
     if (q0 + k < NQ) dg_eflux_point<NQ>(nx, ny, m, t[k], r + pa[k]);
 }
 
+// ---- field-lane volume items: operator tables as constant-bank operands ------------
+// One lane per (cell, field f < 5): the lane reads the ND values of its field
+// once and applies every row of S_r and S_s to them.  The operator entries are
+// then the same for all lanes, so they come from the constant bank as DFMA
+// operands (no load instruction, no shared-memory or L1 traffic): a cell costs
+// 5 x ND/2 16-byte shared loads instead of 10 lanes x 5 ND/2 broadcast loads
+// plus ND^2 table loads.  The five fields of a cell sit in adjacent lanes of
+// one warp (6 cells per warp, lanes 30-31 idle); the output field g needs one
+// x- and one y-derivative of two other fields, fetched with two shuffles per
+// DoF.  Same products and sums per value as dg_vol (j ascending).
+// The tables are mirrored from the kernel's parameter block before every launch
+// (refresh_const_tables); one mirror per degree.
+__constant__ double c_dg_vol_p1[2 * 3 * 3];
+__constant__ double c_dg_vol_p2[2 * 6 * 6];
+__constant__ double c_dg_vol_p3[2 * 10 * 10];
+__constant__ double c_dg_vol_p4[2 * 15 * 15];
+
+template <int P>
+__device__ __forceinline__ double dg_cvol(int k) {
+  if constexpr (P == 1) return c_dg_vol_p1[k];
+  else if constexpr (P == 2) return c_dg_vol_p2[k];
+  else if constexpr (P == 3) return c_dg_vol_p3[k];
+  else return c_dg_vol_p4[k];
+}
+
+// f: the lane's field (0 vx, 1 vy, 2 sxx, 3 syy, 4 sxy); base: first lane of the
+// cell's five; valid: the lane owns a cell of the list (others only shuffle)
+template <int P, class C>
+__device__ __forceinline__ void dg_vol_f(C &c, int f, int base, bool valid) {
+  constexpr int ND = DGShape<P>::ND;
+  const double *gm = c.rd(0), *m = c.rd(1);
+  const double *col = f < 2 ? c.rd(2) + f * ND : c.rd(3) + (f - 2) * ND;
+  double F[ND];
+  if (dg_pairs_g<ND>(col, col)) {
+#pragma unroll
+    for (int j = 0; j < ND - 1; j += 2) {
+      const double2 v = ld2(col + j);
+      F[j] = v.x;
+      F[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) F[j] = col[j];
+  }
+  const double rx = gm[0], ry = gm[1], sx = gm[2], sy = gm[3], det = gm[4];
+  const double lam = m[1], mu = m[2], l2m = lam + 2.0 * mu;
+  double dx[ND], dy[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      a += dg_cvol<P>(i * ND + j) * F[j];
+      b += dg_cvol<P>(ND * ND + i * ND + j) * F[j];
+    }
+    dx[i] = rx * a + sx * b;
+    dy[i] = ry * a + sy * b;
+  }
+  // output g = f:  ru_x = det (dx[sxx] + dy[sxy])      ru_y = det (dx[sxy] + dy[syy])
+  //   rs_xx = det (l2m dx[vx] + lam dy[vy])   rs_yy = det (lam dx[vx] + l2m dy[vy])
+  //   rs_xy = det mu (dy[vx] + dx[vy])
+  const int sxl = (base + (f == 0 ? 2 : f == 1 ? 4 : f == 4 ? 1 : 0)) & 31;
+  const int syl = (base + (f == 0 ? 4 : f == 1 ? 3 : f == 4 ? 0 : 1)) & 31;
+  const double cx = f == 2 ? l2m : f == 3 ? lam : 1.0;
+  const double cy = f == 2 ? lam : f == 3 ? l2m : 1.0;
+  const double sc = f == 4 ? det * mu : det;
+  double *out = f < 2 ? c.wr(4) + f * ND : c.wr(5) + (f - 2) * ND;
+  double o[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    const double X = __shfl_sync(0xffffffffu, dx[i], sxl);
+    const double Y = __shfl_sync(0xffffffffu, dy[i], syl);
+    o[i] = f < 2 || f == 4 ? sc * (f == 4 ? Y + X : X + Y) : sc * (cx * X + cy * Y);
+  }
+  if (!valid) return;
+  if (dg_pairs_g<ND>(out, out)) {
+#pragma unroll
+    for (int i = 0; i < ND - 1; i += 2)
+      *reinterpret_cast<double2 *>(out + i) = make_double2(o[i], o[i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < ND; ++i) out[i] = o[i];
+  }
+}
+
 // inverse mass / forward Euler as (cell, field f < 5) items: the ND values of
 // one field, contiguous in the cell's row (16-byte pairs when ND is even)
 template <int P, class C>

@@ -991,7 +991,19 @@ __device__ __forceinline__ void run_tile(const StagedParams &P, int t, double *s
           LT_TACC(8 + (j < 24 ? j : 23), t_loop);
           continue;
         }
-        if (which == 0 && (LT_GROUPED & 1))
+        if (which == 0 && (LT_GROUPED & 16)) {
+          // field lanes: 6 cells x 5 fields per warp, warp-uniform trip count
+          // (every lane takes part in the shuffles)
+          const int lane = threadIdx.x & 31, cw = lane / 5, f = lane - 5 * cw;
+          constexpr int kCells = 6 * (LT_SBLOCK / 32);
+          for (int c0 = 6 * (threadIdx.x >> 5); c0 - 6 * (int)(threadIdx.x >> 5) < n;
+               c0 += kCells) {
+            const bool valid = cw < 6 && c0 + cw < n;
+            StagedCtxT<RES> cx{L, 0, valid ? c0 + cw : n - 1, 0, scratch, Dd, smem, base, B,
+                               LH + 2};
+            dg_vol_f<PP>(cx, f, lane - f, valid);
+          }
+        } else if (which == 0 && (LT_GROUPED & 1))
           for_flat(n, DGGroup<PP>::GV, [&](int pos, int g) {
             StagedCtxT<RES> cx{L, 0, pos, 0, scratch, Dd, smem, base, B, LH + 2};
             dg_vol_g<PP>(cx, g);
@@ -3102,6 +3114,26 @@ static std::shared_ptr<ExecPlan> build_plan(Ctx &ctx, lt_schedule *s, const Chai
   return plan;
 }
 
+// Mirror the volume kernels' operator tables into the constant bank (field-lane
+// volume items read them as instruction operands).  Device-to-device on the
+// execution stream before every launch: in-place parameter updates and captured
+// graphs see current values.  One mirror per degree and process: contexts that
+// run the same degree with different tables must not execute concurrently.
+static void refresh_const_tables(Ctx &ctx, const ExecPlan &P) {
+  for (const DLoop &L : P.host_loops) {
+    const int k = L.kernel - K_DG_FIRST;
+    if (k < 0 || k % 5 != 0 || !L.params) continue;
+    const int p = k / 5 + 1, nd = dg_nd(p);
+    const size_t bytes = sizeof(double) * 2 * nd * nd;
+    const void *sym = p == 1   ? (const void *)c_dg_vol_p1
+                      : p == 2 ? (const void *)c_dg_vol_p2
+                      : p == 3 ? (const void *)c_dg_vol_p3
+                               : (const void *)c_dg_vol_p4;
+    LT_CK(cudaMemcpyToSymbolAsync(sym, L.params, bytes, 0, cudaMemcpyDeviceToDevice,
+                                  ctx.stream));
+  }
+}
+
 typedef void (*StagedFn)(const StagedParams, const int32_t *);
 static StagedFn staged_fn(int fam) {
   switch (fam) {
@@ -3324,6 +3356,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
       ++launches;
     }
     if (D.n_items > 0) {
+      refresh_const_tables(ctx, P);
       dataflow_fn(fam, P.wide)<<<std::min(P.grid, D.n_items), LT_SBLOCK, P.smem_bytes, ctx.stream>>>(
           sp, D);
       LT_CK_LAUNCH();
@@ -3332,6 +3365,7 @@ static void execute_tiled(Ctx &ctx, lt_schedule *s, const ChainView &cv, const l
     }
     colors = (int)P.phases.size();
   } else {
+    if (P.staged && !dry) refresh_const_tables(ctx, P);
     for (int r = 0; r < repeats; ++r) {
       for (size_t ph = 0; ph < P.phases.size(); ++ph) {
         const int reg = P.phase_region[ph];
