@@ -1787,8 +1787,13 @@ static std::string plan_key(const Ctx &ctx, const ChainView &cv, const lt_arg *a
 static const size_t kSmemBudget = 96 * 1024;
 // shared scratch for one chunk of INC contributions in the staged executor
 // (smaller chunks: more apply phases, more resident tiles per SM)
+// First-pass record/contribution scratch per CTA.  LT_SCRATCH_KB fixes it (and
+// switches the later planning passes off); LT_SCRATCH1_KB only sets the first
+// pass, i.e. the shortest chunk any tile gets and the shared memory the
+// occupancy target is derived from (per-tile chunks still grow from there).
 static size_t scratch_budget() {
   const char *e = getenv("LT_SCRATCH_KB");
+  if (!e) e = getenv("LT_SCRATCH1_KB");
   return (e ? (size_t)atoi(e) : 8) * 1024;
 }
 static std::string g_last_fit;
