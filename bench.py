@@ -60,6 +60,8 @@ def parse(argv=None):
     ap.add_argument("--stated-ts", action="store_true",
                     help="also time the configuration's stated seed tile (config 3: 4096)")
     ap.add_argument("--chains", type=int, default=None, help="chains per step")
+    ap.add_argument("--renumber", default=None,
+                    help="layout pass of the device generator: none, morton, block:BXxBY")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -419,6 +421,8 @@ def main(argv=None):
         over["ts"] = args.ts
     if args.chains:
         over["chains_per_step"] = args.chains
+    if args.renumber:
+        over["renumber"] = None if args.renumber == "none" else args.renumber
     w = W.workload(args.config, **over)
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:

@@ -339,7 +339,7 @@ def rect_mesh_device(nx: int, ny: int, device) -> dict:
     return {"nv": nv, "c2v": c2v, "if2c": if2c, "iface": iface, "ef2c": one, "eface": oneface}
 
 
-def morton_renumber_device(m: dict, nx: int, ny: int) -> dict:
+def morton_renumber_device(m: dict, nx: int, ny: int, block=None) -> dict:
     """Locality renumbering of a device mesh (north star item 3, the layout
     pass): quads in Morton (Z-curve) order of (i, j), the two cells of a quad
     kept adjacent, so ``ts`` consecutive cells form a compact block of quads
@@ -359,7 +359,16 @@ def morton_renumber_device(m: dict, nx: int, ny: int) -> dict:
             out |= ((v >> k) & 1) << (2 * k)
         return out
 
-    code = spread(q % nx) | (spread(q // nx) << 1)
+    if block is None:
+        code = spread(q % nx) | (spread(q // nx) << 1)
+    else:
+        # bx x by blocks of quads, blocks and the quads inside them row-major:
+        # 2*bx*by consecutive cells are one block (seed tiles of any such size)
+        bx, by = block
+        qi, qj = q % nx, q // nx
+        nbx = (nx + bx - 1) // bx
+        code = ((qj // by) * nbx + qi // bx) * (bx * by) + (qj % by) * bx + qi % bx
+        del qi, qj
     qs = torch.argsort(code)
     del code, q
     old_of_new = torch.stack([2 * qs, 2 * qs + 1], dim=1).reshape(-1)
@@ -447,6 +456,10 @@ def elastic_setup_device(nx: int, ny: int, p: int, steps_per_chain: int = 1,
     old_of_new = None
     if renumber == "morton":
         m = morton_renumber_device(m, nx, ny)
+        old_of_new = m.pop("old_of_new")
+    elif isinstance(renumber, str) and renumber.startswith("block:"):   # "block:3x2"
+        bx, by = (int(v) for v in renumber[6:].split("x"))
+        m = morton_renumber_device(m, nx, ny, block=(bx, by))
         old_of_new = m.pop("old_of_new")
     elif renumber not in (None, "none"):
         raise ValueError(f"unknown device renumbering {renumber!r}")

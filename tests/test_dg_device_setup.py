@@ -58,12 +58,14 @@ def test_device_map_validation():
         MeshMap("m", a, b, 2, torch.tensor([0, 1, 2]))
 
 
-@pytest.mark.parametrize("nx,ny,p,T,material,noise", [
-    (6, 4, 1, 1, "homogeneous", 1),
-    (8, 8, 2, 2, ("uniform", 2), 1),
-    (5, 3, 3, 1, ("uniform", 7), None),
+@pytest.mark.parametrize("nx,ny,p,T,material,noise,scheme", [
+    (6, 4, 1, 1, "homogeneous", 1, "morton"),
+    (8, 8, 2, 2, ("uniform", 2), 1, "morton"),
+    (5, 3, 3, 1, ("uniform", 7), None, "morton"),
+    (8, 6, 2, 1, ("uniform", 4), 3, "block:4x3"),
+    (7, 5, 1, 2, "homogeneous", 1, "block:4x2"),
 ])
-def test_morton_renumbering_is_a_consistent_permutation(nx, ny, p, T, material, noise):
+def test_morton_renumbering_is_a_consistent_permutation(nx, ny, p, T, material, noise, scheme):
     """The layout pass (north star item 3) permutes cells and facets and changes
     nothing else: per-cell inputs follow their cells, every facet still joins
     the same two cells through the same faces, and the oracle's untiled chain
@@ -74,12 +76,18 @@ def test_morton_renumbering_is_a_consistent_permutation(nx, ny, p, T, material, 
     a = elastic_setup_device(nx, ny, p, T, material=material, noise_seed=noise, sigma=2.0,
                              device="cpu")
     b = elastic_setup_device(nx, ny, p, T, material=material, noise_seed=noise, sigma=2.0,
-                             device="cpu", renumber="morton")
-    old_of_new = morton_renumber_device(rect_mesh_device(nx, ny, "cpu"), nx, ny)["old_of_new"]
+                             device="cpu", renumber=scheme)
+    block = None if scheme == "morton" else tuple(int(v) for v in scheme[6:].split("x"))
+    old_of_new = morton_renumber_device(rect_mesh_device(nx, ny, "cpu"), nx, ny,
+                                        block=block)["old_of_new"]
     old_of_new = old_of_new.numpy()
     assert sorted(old_of_new.tolist()) == list(range(2 * nx * ny))
-    # first ts cells form a compact block: 16 consecutive cells = 4 x 2 quads
-    if nx >= 4 and ny >= 2:
+    if block is not None:  # the first 2*bx*by cells are the bx x by block of quads at the origin
+        bx, by = block
+        quads = sorted(set(int(c) // 2 for c in old_of_new[:2 * bx * by]))
+        assert {(q % nx, q // nx) for q in quads} == {(i, j) for i in range(bx) for j in range(by)}
+    # Morton: 16 consecutive cells = 4 x 2 quads
+    elif nx >= 4 and ny >= 2:
         quads = sorted(set(int(c) // 2 for c in old_of_new[:16]))
         assert {(q % nx, q // nx) for q in quads} == {(i, j) for i in range(4) for j in range(2)}
     for name in ("cgeo", "mat", "u", "s"):
