@@ -9,7 +9,7 @@ Workloads (``paper_1708_03183_b200/workloads.py``, BASELINE.json configs):
   cells, 3.36e9 DoFs), homogeneous, Gaussian pulse, two timesteps per chain
   -- the largest elastic-wave configuration and the one BASELINE strong-scales
   over 1/2/4/8 GPUs.  Generated on the GPU (no host pass over the mesh), cells
-  numbered along a Z-curve by the layout pass (``renumber: morton``).
+  numbered block by block (4x3 quads per seed tile) by the layout pass (``renumber``).
 * config 3: DG P2 2048x2048, heterogeneous, two timesteps per chain
   (``--stated-ts`` also times BASELINE's seed tile 4096).
 * config 2: DG P1 256x256, one timestep per chain, 10 chains per step.

@@ -14,13 +14,15 @@ exactly the same problem, schedule and runner:
 
 ``ts`` is the seed tile the B200 executor is tuned for (one tile per CTA,
 footprint in shared memory); ``ts_stated`` the configuration's own seed tile
-where BASELINE states one.  ``renumber`` is the layout pass of the device
-generator (north star item 3): "morton" numbers quads along a Z-curve, so a
-seed tile of 16 / 32 cells is a 4x2 / 4x4 block of quads instead of a
-one-quad-high strip of the row-major numbering (measured: config 3 12.89 ->
-12.12 ms, config 4 169.6 -> 162.6 ms per chain).  Inputs larger than a few million cells are
-generated on the GPU (``dg.elastic_setup_device``: same numbering and draws as
-the host generator, tests/test_dg_device_setup.py).
+where BASELINE states one.  ``renumber`` is the layout pass of the device generator (north star item 3):
+"block:BXxBY" numbers the quads block by block (BX x BY quads, blocks and the
+quads inside them row-major), "morton" along a Z-curve, so a seed tile of
+2*BX*BY consecutive cells is one compact block of quads instead of a
+one-quad-high strip of the row-major numbering: smaller footprints after
+projection across the chain, 5 colours instead of 7.  Measured per chain
+(B200): config 3 row-major ts 24 12.89 ms, Morton ts 32 10.92, block 4x4 ts 32
+10.77; config 4 row-major ts 12 169.6 ms, Morton ts 16 162.6, block 4x2 ts 16
+158.7, block 4x3 ts 24 157.7 (`profiles/r02_sweep_block_renumbering.txt`).
 """
 
 from __future__ import annotations
@@ -47,7 +49,7 @@ class Workload:
     chains_per_step: int        # chains one bench step executes
     device_setup: bool
     text: str
-    renumber: str | None = None  # layout pass of the device generator: None or "morton"
+    renumber: str | None = None  # layout pass of the device generator: None, "morton", "block:BXxBY"
 
     @property
     def cells(self) -> int:
@@ -71,12 +73,12 @@ CONFIGS = {
                 job_chains=50, chains_per_step=1, device_setup=True,
                 text="config 3: elastic DG P2 2048x2048 (8,388,608 cells), per-cell "
                      "rho,lambda,mu ~ U[1,2] (seed 2), 2 timesteps/chain",
-                renumber="morton"),
-    4: Workload(4, 8192, 4096, 3, 2, "homogeneous", None, 8.0, ts=16, ts_stated=None,
+                renumber="block:4x4"),
+    4: Workload(4, 8192, 4096, 3, 2, "homogeneous", None, 8.0, ts=24, ts_stated=None,
                 job_chains=25, chains_per_step=1, device_setup=True,
                 text="config 4: elastic DG P3 8192x4096 (67,108,864 cells), homogeneous, "
                      "Gaussian pulse, 2 timesteps/chain",
-                renumber="morton"),
+                renumber="block:4x3"),
 }
 
 

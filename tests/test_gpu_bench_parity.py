@@ -10,12 +10,12 @@ for the step's chains) captured in a CUDA graph, as bench.py runs it.
   the fields within 1e-12 (normwise, reference executor.py:163-169 is
   "untiled sequential execution").
 * config 3 at full size (2048x2048 P2, heterogeneous, T=2) as benchmarked
-  (Morton layout pass, seed tile 32), at BASELINE's stated seed tile 4096 and in
-  the generator's row-major numbering (seed tile 24): tiled == GPU untiled
+  (block 4x4 layout pass, seed tile 32), at BASELINE's stated seed tile 4096, in
+  the Morton numbering (32) and the generator's row-major numbering (24): tiled == GPU untiled
   (itself pinned to the reference on the small goldens) within 1e-12, and zero
   legality violations of the schedule at that size.
-* config 4's chain as benchmarked (P3, T=2, homogeneous, no noise, Morton
-  layout pass, seed tile 16) on a 1024x512 cut of the config-4 mesh: tiled ==
+* config 4's chain as benchmarked (P3, T=2, homogeneous, no noise, block 4x3
+  layout pass, seed tile 24) on a 1024x512 cut of the config-4 mesh: tiled ==
   untiled within 1e-12 (the full 67M-cell untiled
   executor does not fit next to the tiled state; bench.py runs the full size).
 """
@@ -91,14 +91,16 @@ def config3_untiled(renumber):
     return _C3_UNTILED[renumber]
 
 
-@pytest.mark.parametrize("renumber,ts", [("morton", 32), ("morton", 4096), (None, 24)])
+@pytest.mark.parametrize("renumber,ts", [("block:4x4", 32), ("block:4x4", 4096),
+                                         ("morton", 32), (None, 24)])
 def test_config3_full_tiled_matches_untiled(renumber, ts):
-    """Bench configuration (Morton layout pass, seed tile 32), BASELINE's stated
-    seed tile 4096, and the generator's row-major numbering at its best tile."""
+    """Bench configuration (block 4x4 layout pass, seed tile 32), BASELINE's
+    stated seed tile 4096, the Morton numbering and the generator's row-major
+    numbering at their best tiles."""
     import torch
     ref = config3_untiled(renumber)
     w = W.workload(3, ts=ts, renumber=renumber)
-    if (renumber, ts) == ("morton", 32):
+    if (renumber, ts) == ("block:4x4", 32):
         assert (w.ts, w.renumber) == (W.workload(3).ts, W.workload(3).renumber)
     pb = W.build_problem(w)
     sched = lt.inspect_chain(pb.chain, ts, lt.ExecMode.SHARED)
