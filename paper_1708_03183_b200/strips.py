@@ -162,7 +162,8 @@ def bench_partitioned(args, w, rank, world, local, bench):
     pb.install_params()
     setup_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    sched = inspect_chain(pb.chain, w.ts, ExecMode.SHARED)
+    ts = w.ts_strips or w.ts  # strips keep the generator's row-major numbering
+    sched = inspect_chain(pb.chain, ts, ExecMode.SHARED)
     inspect_s = time.perf_counter() - t0
     const = constant_datasets(pb.chain, pb.bindings)
     exchanged = tuple(n for n in exchanged_from_chain(pb.chain, pb.bindings) if n not in const)
@@ -227,7 +228,8 @@ def bench_partitioned(args, w, rank, world, local, bench):
             "data": "synthetic",
             "config": {"workload": w.text + f"; {world} contiguous strips, halo depth {depth}",
                        "p": w.p, "cells": w.cells, "dofs": w.dofs, "timesteps_per_chain": w.T,
-                       "chains_per_step": chains, "seed_tile": w.ts, "mode": "shared (mixed)",
+                       "chains_per_step": chains, "seed_tile": ts, "renumber": "none",
+                       "mode": "shared (mixed)",
                        "rank0_cells_local": loc.spaces[CELLS].total, "rank0_cells_owned": owned,
                        "colors_rank0": len(sched.color_order), "setup_s": round(setup_s, 1),
                        "inspect_s": round(inspect_s, 3),

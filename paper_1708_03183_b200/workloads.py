@@ -50,6 +50,7 @@ class Workload:
     device_setup: bool
     text: str
     renumber: str | None = None  # layout pass of the device generator: None, "morton", "block:BXxBY"
+    ts_strips: int | None = None  # seed tile of the partitioned path (row-major strip numbering)
 
     @property
     def cells(self) -> int:
@@ -78,7 +79,7 @@ CONFIGS = {
                 job_chains=25, chains_per_step=1, device_setup=True,
                 text="config 4: elastic DG P3 8192x4096 (67,108,864 cells), homogeneous, "
                      "Gaussian pulse, 2 timesteps/chain",
-                renumber="block:4x3"),
+                renumber="block:4x3", ts_strips=12),
 }
 
 
