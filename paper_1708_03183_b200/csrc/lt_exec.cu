@@ -272,9 +272,12 @@ __device__ __forceinline__ void for_flat(int cnt, int groups, F &&f) {
 // one facet point per lane) win for the contractions -- grouped volume, records
 // and apply items are 40-70 % slower per phase at P3 despite 3x fewer shared
 // loads -- while the per-field inverse-mass/update items are 20 % faster
-// (conflict-free 16-byte rows); at P2 grouped volume + apply also gain 1.7 %.
+// (conflict-free 16-byte rows).  At the bench configurations (block layout, 3-4
+// CTAs/SM) grouped volume items gain 2.6 % at P2 (mask 9: 10.78 -> 10.50 ms) and
+// grouped apply items 0.9 % at P3 (mask 12: 39.46 -> 39.10 ms on the config 4
+// cut); profiles/r02_ab_masks_final_config.txt.
 // (evaluated inside run_tile<FAM, ...>)
-#define LT_GROUPED (FAM == 2 ? 13 : 8)
+#define LT_GROUPED (FAM == 2 ? 9 : FAM == 3 ? 12 : 8)
 #endif
 
 // ---- fused tiled executor ------------------------------------------------------

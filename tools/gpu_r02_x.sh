@@ -1,6 +1,6 @@
-# round 2, call x: FINAL-build evidence (block layout pass, 4 KB first-pass scratch): full GPU test suite,
+# round 2, call x (re-run as r02x2 after the work-item masks changed): FINAL-build evidence (block layout pass, 4 KB first-pass scratch): full GPU test suite,
 # bench lines (no profiler), launch lists, ncu --set full of the config 4 / 3 / 2 bench launches, phase cycles
-O=gpurun_out/r02x
+O=gpurun_out/r02x2
 mkdir -p $O
 timeout 2400 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
 python -c 'import __graft_entry__ as g; g.smoke()' > $O/smoke.log 2>&1; tail -1 $O/smoke.log
@@ -8,7 +8,6 @@ timeout 900 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err; tail -c 400 $
 timeout 600 python bench.py --config 3 --stated-ts --steps 5 > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 300 python bench.py --config 2 > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
-timeout 600 python bench.py --partitioned --steps 3 --warmup 3 --no-e2e > $O/bench_c4_partitioned_n1.json 2> $O/bench_c4_partitioned_n1.err
 for c in 4 3 2; do
 timeout 900 python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-omega > $O/plain_c$c.json 2> $O/plain_c$c.err && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_dataflow|k_pack_ro|FillFunctor' -c 40 --csv --log-file $O/launches_c$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-omega > $O/ncu_launch_c$c.log 2>&1
