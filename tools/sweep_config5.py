@@ -30,6 +30,11 @@ from paper_1708_03183_b200.executor import UntiledRunner
 
 GLOBAL = {1: (8192, 8192), 2: (8192, 4096), 3: (4480, 4480), 4: (3648, 3648)}
 TUNE = {1: (24, 32, 48), 2: (12, 16, 24), 3: (8, 12, 16), 4: (6, 8, 12)}
+# --layout block: every seed tile is one block of quads of the layout pass
+# (dg.morton_renumber_device, "block:BXxBY" with 2*BX*BY = ts)
+TUNE_BLOCK = {1: ((32, "4x4"), (48, "6x4"), (16, "4x2")), 2: ((32, "4x4"), (24, "4x3"), (16, "4x2")),
+              3: ((24, "4x3"), (16, "4x2"), (8, "2x2")), 4: ((16, "4x2"), (12, "3x2"), (8, "2x2"))}
+STATED_BLOCK = {1024: "32x16", 4096: "64x32", 16384: "128x64"}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--degrees", default="1,2,3,4")
@@ -37,6 +42,7 @@ ap.add_argument("--chains", default="1,2,4")
 ap.add_argument("--stated", default="1024,4096,16384")
 ap.add_argument("--timesteps", type=int, default=4, help="timesteps timed per point")
 ap.add_argument("--out", default=None)
+ap.add_argument("--layout", default="none", choices=["none", "block"])
 a = ap.parse_args()
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 stream = torch.cuda.current_stream()
@@ -74,9 +80,21 @@ for p in (int(v) for v in a.degrees.split(",")):
         base = {"p": p, "T": T, "mesh": f"{gx}x{gy // 8}", "cells": w.cells, "dofs": w.dofs,
                 "untiled_ms_per_chain": round(u_s * 1e3, 3), "untiled_value": upd / u_s,
                 "setup_s": round(setup_s, 1)}
-        for kind, tss in (("tuned", TUNE[p]), ("stated", [int(v) for v in a.stated.split(",")])):
-            for ts in tss:
+        if a.layout == "block":
+            points = [("tuned", ts, b) for ts, b in TUNE_BLOCK[p]] + \
+                     [("stated", int(v), STATED_BLOCK[int(v)]) for v in a.stated.split(",")]
+        else:
+            points = [("tuned", ts, None) for ts in TUNE[p]] + \
+                     [("stated", int(v), None) for v in a.stated.split(",")]
+        for kind, ts, blk in points:
+            if True:
                 try:
+                    if blk is not None:  # the layout is part of the problem: rebuild it
+                        pb = None
+                        torch.cuda.empty_cache()
+                        from dataclasses import replace
+                        pb = W.build_problem(replace(w, renumber="block:" + blk))
+                        base["layout"] = "block:" + blk
                     t0 = time.perf_counter()
                     s = lt.inspect_chain(pb.chain, ts, lt.ExecMode.SHARED)
                     insp = time.perf_counter() - t0
@@ -94,5 +112,5 @@ for p in (int(v) for v in a.degrees.split(",")):
                 except Exception as e:
                     emit(dict(base, kind=kind, ts=ts, error=str(e).splitlines()[0][:200]))
                 torch.cuda.empty_cache()
-        del pb
+        pb = None
         torch.cuda.empty_cache()
