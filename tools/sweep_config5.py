@@ -15,6 +15,7 @@ chosen per (P, T) from a short sweep.  Each point checks legality
 usage: python tools/sweep_config5.py [--degrees 1,2,3,4] [--chains 1,2,4] [--out FILE]
 """
 import argparse
+import gc
 import json
 import os
 import sys
@@ -91,6 +92,7 @@ for p in (int(v) for v in a.degrees.split(",")):
                 try:
                     if blk is not None:  # the layout is part of the problem: rebuild it
                         pb = None
+                        gc.collect()  # problems hold reference cycles: free their tensors now
                         torch.cuda.empty_cache()
                         from dataclasses import replace
                         pb = W.build_problem(replace(w, renumber="block:" + blk))
